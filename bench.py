@@ -1,0 +1,349 @@
+"""Benchmark: scheduling instances solved per second on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2|C3|C4|C5]
+    python bench.py --impl reference ...     # the CPU oracle, timed on the host cores
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = one pass of the whole hot path (descriptor
+load, prefix/quantise, EDF sort, DP sweep, backtrack, schedule, stats) over
+one batch of the configuration's instances, inputs resident in HBM (each rank
+generates its own global-id shard on device; weak scaling: every rank solves
+a full batch), followed by the NCCL all-reduce of the int64 stats vector when
+N > 1.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+SMEM_BYTES_PER_CLK_PER_SM = 128  # LDS crossbar (B300_MICROARCH.md "smem crossbar BW 128/N B/cyc/SM")
+BYTES_PER_EVAL = 4               # one int32 DP cell read per (task, tick, option)
+METRIC = "scheduling instances solved/sec"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def _sms():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def algorithmic_evals(inputs, n_tasks, opt_stride, chunk=65536):
+    """W = sum_i [(T+1) + sum_k #{t <= d_i : t - C_i(k) >= r_i}] per instance,
+    T = max(0, max_i d_i).  Measurement only (torch ops on the generated inputs)."""
+    import torch
+    B = inputs["task_begin"].numel() - 1
+    total = 0
+    for lo in range(0, B, chunk):
+        hi = min(B, lo + chunk)
+        sl = slice(lo * n_tasks, hi * n_tasks)
+        m = inputs["mand_wcet"][sl].long()
+        ow = inputs["opt_wcet"][sl].long()
+        S = inputs["n_opt"][sl].long()
+        w = torch.cat([m[:, None], ow], 1)
+        C = torch.cumsum(w, 1)
+        k = torch.arange(opt_stride + 1, device=C.device)[None, :]
+        valid = k <= S[:, None]
+        d = inputs["deadline"][sl].long()
+        r = inputs["release"][sl].long()
+        cnt = torch.clamp(d[:, None] - r[:, None] - C + 1, min=0) * valid
+        T = torch.clamp(d.view(-1, n_tasks).max(1).values, min=0)
+        total += int(((T + 1) * n_tasks).sum() + cnt.sum())
+    return total
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload_config(cw, args, n_instances):
+    mode = f"Delta={args.delta_micro / 1e6:g}" if args.delta_micro else f"FPTAS eps={cw.epsilon_micro / 1e6:g}"
+    return {"workload": f"{cw.name}: {n_instances} instances/GPU x {cw.n_tasks} tasks x (1 mandatory + "
+                        f"{cw.n_opt} optional stages), horizon {cw.horizon} ticks, U in [{cw.u_lo},{cw.u_hi}], "
+                        f"{mode}, drop allowed",
+            "name": cw.name, "instances_per_gpu": n_instances, "tasks": cw.n_tasks, "optional_stages": cw.n_opt,
+            "horizon": cw.horizon, "seed": hex(cw.seed)}
+
+
+def cpu_oracle_rate(cw, args, target_s):
+    """The oracle as it stands (paper DP, OpenMP over instances) on a bounded sample."""
+    import oracle
+    threads = os.cpu_count() or 1
+    ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
+                               max_tasks=cw.n_tasks, max_horizon=cw.horizon)
+    probe = gen.generate(cw, max(threads * 2, 16))
+    t0 = time.perf_counter()
+    oracle.solve(probe, ocfg, oracle.PAPER, threads)
+    dt = max(time.perf_counter() - t0, 1e-4)
+    n = int(min(cw.n_instances, max(probe.n_instances, probe.n_instances * target_s / dt)))
+    sample = gen.generate(cw, n, id_offset=probe.n_instances)
+    t0 = time.perf_counter()
+    oracle.solve(sample, ocfg, oracle.PAPER, threads)
+    el = time.perf_counter() - t0
+    return n / el, n, el, threads
+
+
+def run_reference(args, cw, rank, world):
+    """--impl reference: the CPU oracle (paper DP) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    threads = os.cpu_count() or 1
+    ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
+                               max_tasks=cw.n_tasks, max_horizon=cw.horizon)
+    # size each step for ~3 s of CPU work so K+W steps stay within a few minutes
+    probe = gen.generate(cw, max(threads * 2, 16))
+    t0 = time.perf_counter()
+    oracle.solve(probe, ocfg, oracle.PAPER, threads)
+    per = max(time.perf_counter() - t0, 1e-4) / probe.n_instances
+    n = int(min(cw.n_instances, max(threads, 3.0 / per)))
+    sample = gen.generate(cw, n)
+    for _ in range(args.warmup):
+        oracle.solve(sample, ocfg, oracle.PAPER, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.solve(sample, ocfg, oracle.PAPER, threads)
+    el = time.perf_counter() - t0
+    v = n * args.steps / el
+    line = {"metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "impl": "reference", "config": workload_config(cw, args, n),
+            "cpu_baseline": {"value": v, "unit": "instances/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{n} instances of {cw.name} per step, paper reward-indexed DP (O2)"},
+            "e2e": {"value": v, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--instances", type=int, default=0, help="override instances per GPU")
+    ap.add_argument("--delta-micro", type=int, default=0, help="fixed Delta instead of FPTAS eps")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    cw = gen.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        run_reference(args, cw, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2011_01112_b200 as pkg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_inst = args.instances or (cw.u_blocks and cw.n_instances // max(world, 1)) or cw.n_instances
+    id0 = rank * n_inst
+    stream = torch.cuda.Stream(dev)
+
+    # ---- inputs resident in HBM: this rank's global-id shard, generated on device
+    with torch.cuda.stream(stream):
+        if cw.u_blocks:
+            parts, start = [], 0
+            for u, cnt in cw.u_blocks:
+                lo, hi = max(id0, start), min(id0 + n_inst, start + cnt)
+                if lo < hi:
+                    g = cw.gen_config(None, u, u)
+                    parts.append(pkg.gen_batch_device(g.seed, g.n_tasks, g.n_opt, g.opt_stride, g.horizon,
+                                                      g.u_lo_q16, g.u_hi_q16, g.d_lo, hi - lo, lo,
+                                                      device=dev, stream=stream))
+                start += cnt
+            inputs = {k: torch.cat([p[k] if k != "task_begin" else p[k][:-1] + i * 0 for i, p in enumerate(parts)])
+                      for k in parts[0]}
+            inputs["task_begin"] = torch.arange(n_inst + 1, device=dev, dtype=torch.int64) * cw.n_tasks
+        else:
+            g = cw.gen_config()
+            inputs = pkg.gen_batch_device(g.seed, g.n_tasks, g.n_opt, g.opt_stride, g.horizon, g.u_lo_q16,
+                                          g.u_hi_q16, g.d_lo, n_inst, id0, device=dev, stream=stream)
+    stream.synchronize()
+    T = n_inst * cw.n_tasks
+    in_bytes = sum(v.numel() * v.element_size() for v in inputs.values())
+    W = algorithmic_evals(inputs, cw.n_tasks, cw.n_opt)
+
+    sc = pkg.SchedConfig(device=local, max_tasks=cw.n_tasks, max_opt_stages=cw.n_opt, max_horizon=cw.horizon,
+                         delta_micro=args.delta_micro, epsilon_micro=cw.epsilon_micro)
+    sched = pkg.Scheduler(sc)
+    info = sched.info()
+    out = pkg.alloc_outputs(n_inst, T, device=dev)
+    out_bytes = sum(v.numel() * v.element_size() for k, v in out.items() if k != "stats")
+
+    def step():
+        out["stats"].zero_()
+        sched.solve_batch(inputs, out, stream)
+        if world > 1:
+            dist.all_reduce(out["stats"])
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+        t_start.record(stream)
+        for i in range(args.steps):
+            out["stats"].zero_()
+            ev[i][0].record(stream)
+            sched.solve_batch(inputs, out, stream)
+            ev[i][1].record(stream)
+            if world > 1:
+                dist.all_reduce(out["stats"])
+        t_end.record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize(dev)
+    ms = t_start.elapsed_time(t_end)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    tmax = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = float(tmax.item())
+    stats = out["stats"].cpu().numpy()
+    value = n_inst * world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public host-buffer entry point (pinned H2D + solve + D2H)
+    e2e = None
+    if not args.no_e2e:
+        hin = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in inputs.items()}
+        for k in hin:
+            hin[k].copy_(inputs[k])
+        hout = pkg.alloc_outputs(n_inst, T, host=True, pinned=True)
+        for _ in range(2):
+            sched.solve_batch_host(hin, hout, stream)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(2, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(ke):
+            sched.solve_batch_host(hin, hout, stream)
+        e1.record(stream)
+        e1.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1) / ke], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_inst * world / (float(ems.item()) / 1e3), "unit": "instances/s",
+               "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(out_bytes + 64)}
+
+    if rank == 0:
+        peaks = _peaks()
+        sms = _sms()
+        clk_s = clk.summary()
+        fmax = peaks.get("sm_max_mhz") or clk_s.get("sm_max_mhz") or 1965.0
+        peak_gbs = SMEM_BYTES_PER_CLK_PER_SM * sms * fmax * 1e6 / 1e9
+        achieved = W * BYTES_PER_EVAL / (kern_ms / 1e3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"ncu_{cw.name}_summary.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic (device-generated, seeded)",
+            "config": dict(workload_config(cw, args, n_inst),
+                           l2=f"inputs {in_bytes / 1e6:.0f} MB/GPU vs L2 126 MB" +
+                              (" (larger than L2)" if in_bytes > 126e6 else " (fits L2; not flushed)"),
+                           parallelism=f"instance shards x{world}"),
+            "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                         "frac": achieved / peak_gbs, "traffic": traffic,
+                         "peak_basis": f"128 B/clk/SM LDS x {sms} SMs x {fmax:.0f} MHz (guide-derived; no "
+                                       "measured smem peak in MEASURED_PEAKS.json)",
+                         "evals_per_instance": W / n_inst, "kernel_ms": kern_ms},
+            "gpu_launches": args.steps,
+            "clocks": clk_s,
+            "kernel": info,
+            "stats": dict(zip(pkg.STATS_FIELDS, [int(x) for x in stats])),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            v, n, el, thr = cpu_oracle_rate(cw, args, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": "instances/s", "cores": thr, "kind": "oracle",
+                                    "sample": f"{n} {cw.name} instances (ids after the probe), paper "
+                                              f"reward-indexed DP (O2), {el:.1f} s"}
+        print(json.dumps(line), flush=True)
+    sched.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,125 @@
+/* ic_sched.h — C ABI of the batched confidence-maximising depth assignment.
+ *
+ * The operation (PAPER.md = P, SPEC.md = S; P:Lnn = line nn):
+ *   Each instance is a task set J(t).  Task i is an imprecise
+ *   computation: a mandatory block of m_i ticks with confidence a_i0,
+ *   followed by S_i optional stages with WCETs c_ik (P:L48 p_il) and
+ *   confidence gains g_ik, so that R_i(k) = a_i0 + sum_{j<=k} g_ij is the
+ *   confidence after k optional stages (P:L48 R_i^L) and
+ *   C_i(k) = m_i + sum_{j<=k} c_ij its cumulative WCET (P:L48 P_i^L).
+ *   The solver chooses for every task k_i in {dropped, 0..S_i} so that the
+ *   quantised total sum floor(R_i(k_i)/Delta) is maximal while every
+ *   kept task finishes by its (adjusted) deadline when the kept tasks
+ *   run back to back in EDF order — the paper's
+ *   depth assignment, Eqs. 1-2 and Algorithm 1.  Among optimal
+ *   plans it returns the one with the least makespan (Eq. 2's "least amount
+ *   of execution time"), then the smallest depth vector compared from
+ *   the last EDF task backwards, so the result is unique and
+ *   bit-reproducible.
+ *   Delta is fixed (0.1) or the FPTAS step Delta = eps*R/N of
+ *   Theorem 1 with R the best individually feasible reward.
+ *
+ * Units: time in integer ticks; confidence in integer micro-units (1e-6).
+ * EDF order: ascending (deadline, release, index within the instance).
+ * A task starts at max(previous kept finish, release) (reading R9;
+ * with all releases 0 this is exactly the paper's Eq. 2).
+ *
+ * Ownership and calls:
+ *   - All ic_batch_in / ic_batch_out pointers passed to ic_sched_solve_batch
+ *     are CUDA device pointers on the handle's device, owned by the caller.
+ *   - ic_sched_solve_batch is asynchronous and stream-ordered on
+ *     `cuda_stream` (a cudaStream_t; NULL = legacy default stream).  Outputs
+ *     are valid once the stream has synchronised.  One stream at a time per
+ *     handle (the handle's workspace is reused); handles are independent.
+ *   - ic_sched_solve_batch_host takes HOST pointers (pinned memory is
+ *     fastest), copies inputs to handle-owned device staging, solves, copies
+ *     the outputs back and synchronises `cuda_stream` before returning.
+ *
+ * Errors:
+ *   - Host-checkable problems return a negative code immediately and launch
+ *     nothing: IC_ERR_INVALID_ARG (null handle / pointer, bad config),
+ *     IC_ERR_LIMIT (config beyond the compiled limits: max_tasks > 4096,
+ *     max_opt_stages > 14, max_horizon > 32768, or the workspace does not fit
+ *     the device), IC_ERR_CUDA (a CUDA runtime call failed; no device at
+ *     all also reports this), IC_ERR_OOM (workspace allocation failed).
+ *   - Data problems are reported per instance in out->status, never by
+ *     return code: IC_INST_BAD_INPUT when an instance has more than
+ *     max_tasks tasks or a task has n_opt > max_opt_stages, release < 0,
+ *     deadline >= max_horizon, any WCET < 1, mand_conf > 1e6, or a
+ *     cumulative confidence R_i(k) outside [0, 1e6];
+ *     IC_INST_INFEASIBLE when dropping is disallowed and no plan keeps every
+ *     task; IC_INST_LIMIT when 16 * sum_i max_k q_i(k) + 16 * N >= 2^30 (the
+ *     packed 32-bit DP keys would overflow; use a larger Delta).  For all
+ *     three, every kept = -1, start = finish = -1, q_total = conf_micro = 0,
+ *     conf_total = 0.0, makespan = 0.  There is no fallback path.
+ */
+#ifndef IC_SCHED_H
+#define IC_SCHED_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ic_sched ic_sched; /* opaque; owns device workspace, bound to one device */
+
+enum { IC_OK = 0, IC_ERR_INVALID_ARG = -1, IC_ERR_LIMIT = -2, IC_ERR_CUDA = -3, IC_ERR_OOM = -4 };
+enum { IC_DROP_ALLOWED = 0, IC_MANDATORY_ENFORCED = 1 }; /* P:L70 "if dropping entire tasks is disallowed" */
+enum { IC_INST_OK = 0, IC_INST_INFEASIBLE = 1, IC_INST_BAD_INPUT = 2, IC_INST_LIMIT = 3 };
+
+typedef struct {
+  int32_t device;         /* CUDA device ordinal                                         */
+  int32_t drop_mode;      /* IC_DROP_ALLOWED (default, P:L96 skip term) or IC_MANDATORY_ENFORCED */
+  uint32_t delta_micro;   /* > 0: fixed Delta in micro-units (paper default 0.1 -> 100000)   */
+  uint32_t epsilon_micro; /* iff delta_micro == 0: Delta = max(1, floor(eps*R/(1e6*N))),
+                             R = max over tasks/depths with r + C <= d of R_i(k) (Thm 1)    */
+  int32_t max_tasks;      /* N per instance, 1..4096                                        */
+  int32_t max_opt_stages; /* S_i bound and the row stride of opt_wcet/opt_gain, 0..14       */
+  int32_t max_horizon;    /* H: deadlines must be < H; 1..32768                             */
+} ic_sched_config;
+
+typedef struct { /* CSR: instance b owns tasks [task_begin[b], task_begin[b+1]) */
+  int64_t n_instances;
+  const int64_t* task_begin;  /* [B+1], non-decreasing, task_begin[0] is the first task row */
+  const int32_t* release;     /* [T] ticks, >= 0 (earliest start)                          */
+  const int32_t* deadline;    /* [T] ticks, adjusted, inclusive; may be negative     */
+  const int32_t* mand_wcet;   /* [T] ticks >= 1 (the mandatory part as one block, omega = 1) */
+  const uint8_t* n_opt;       /* [T] S_i <= max_opt_stages                                  */
+  const int32_t* opt_wcet;    /* [T][max_opt_stages] ticks >= 1 (first S_i entries used)    */
+  const uint32_t* mand_conf;  /* [T] micro-confidence of the mandatory result, <= 1e6       */
+  const int32_t* opt_gain;    /* [T][max_opt_stages] micro-confidence gain of each stage (may
+                                 be negative: confidence may dip, reading R17)     */
+} ic_batch_in;
+
+typedef struct {
+  int8_t* kept;        /* [T] -1 = dropped (planned miss), else #optional stages kept 0..S_i */
+  int32_t* start;      /* [T] ticks, -1 if dropped                                          */
+  int32_t* finish;     /* [T] ticks, -1 if dropped; finish = start + C_i(kept)               */
+  int64_t* q_total;    /* [B] sum of floor(R/Delta) over kept tasks (the DP objective)       */
+  int64_t* conf_micro; /* [B] sum of R_i(kept) over kept tasks, exact                        */
+  double* conf_total;  /* [B] conf_micro / 1e6                                               */
+  int32_t* makespan;   /* [B] finish of the last kept task (0 if none)                       */
+  uint8_t* status;     /* [B] IC_INST_*                                                      */
+  int64_t* stats;      /* nullable; [8] accumulated (+=) over the batch: instances, tasks of
+                          OK instances, dropped tasks of OK instances, instances not OK,
+                          kept optional stages, offered optional stages (OK instances),
+                          sum conf_micro, sum q_total                                        */
+} ic_batch_out;
+
+int ic_sched_create(const ic_sched_config* cfg, ic_sched** out);
+int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream);
+int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream);
+int ic_sched_destroy(ic_sched* h);
+
+/* Launch geometry chosen at create time (for tests, bench and profiling). */
+typedef struct {
+  int32_t threads_per_cta, cols_per_thread, ctas_per_sm, grid;
+  int32_t smem_bytes, decisions_in_smem, double_buffered, pad_cols;
+  int64_t workspace_bytes;
+} ic_sched_info;
+int ic_sched_get_info(const ic_sched* h, ic_sched_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,223 @@
+"""ctypes marshalling for libicsched.so (include/ic_sched.h, include/ic_gen.h).
+
+Argument marshalling only.  Device memory comes from torch tensors (their
+``data_ptr()``), streams from ``torch.cuda.Stream`` (``cuda_stream``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "libicsched.so")
+
+IC_OK, IC_ERR_INVALID_ARG, IC_ERR_LIMIT, IC_ERR_CUDA, IC_ERR_OOM = 0, -1, -2, -3, -4
+IC_DROP_ALLOWED, IC_MANDATORY_ENFORCED = 0, 1
+IC_INST_OK, IC_INST_INFEASIBLE, IC_INST_BAD_INPUT, IC_INST_LIMIT = 0, 1, 2, 3
+
+# (name, numpy dtype, per "task" | "instance" | "task_opt" | "csr")
+INPUT_FIELDS = (("task_begin", np.int64, "csr"), ("release", np.int32, "task"),
+                ("deadline", np.int32, "task"), ("mand_wcet", np.int32, "task"),
+                ("n_opt", np.uint8, "task"), ("opt_wcet", np.int32, "task_opt"),
+                ("mand_conf", np.uint32, "task"), ("opt_gain", np.int32, "task_opt"))
+OUTPUT_FIELDS = (("kept", np.int8, "task"), ("start", np.int32, "task"), ("finish", np.int32, "task"),
+                 ("q_total", np.int64, "instance"), ("conf_micro", np.int64, "instance"),
+                 ("conf_total", np.float64, "instance"), ("makespan", np.int32, "instance"),
+                 ("status", np.uint8, "instance"))
+STATS_FIELDS = ("instances", "tasks", "dropped", "not_ok", "opt_kept", "opt_offered", "conf_micro",
+                "q_total")
+
+_ERR = {IC_ERR_INVALID_ARG: "invalid argument", IC_ERR_LIMIT: "beyond compiled limits",
+        IC_ERR_CUDA: "CUDA error", IC_ERR_OOM: "out of device memory"}
+
+
+class ICSchedError(RuntimeError):
+    def __init__(self, fn, rc):
+        super().__init__(f"{fn} failed: {rc} ({_ERR.get(rc, 'unknown')})")
+        self.rc = rc
+
+
+class SchedConfig(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("drop_mode", ctypes.c_int32),
+                ("delta_micro", ctypes.c_uint32), ("epsilon_micro", ctypes.c_uint32),
+                ("max_tasks", ctypes.c_int32), ("max_opt_stages", ctypes.c_int32),
+                ("max_horizon", ctypes.c_int32)]
+
+    def __init__(self, device=0, drop_mode=IC_DROP_ALLOWED, delta_micro=0, epsilon_micro=100_000,
+                 max_tasks=64, max_opt_stages=8, max_horizon=4096):
+        super().__init__(device, drop_mode, delta_micro, epsilon_micro, max_tasks, max_opt_stages,
+                         max_horizon)
+
+
+class SchedInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("threads_per_cta", "cols_per_thread", "ctas_per_sm", "grid",
+                                              "smem_bytes", "decisions_in_smem", "double_buffered",
+                                              "pad_cols")] + [("workspace_bytes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class _In(ctypes.Structure):
+    _fields_ = [("n_instances", ctypes.c_int64)] + [(n, ctypes.c_void_p) for n, _, _ in INPUT_FIELDS]
+
+
+class _Out(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n, _, _ in OUTPUT_FIELDS] + [("stats", ctypes.c_void_p)]
+
+
+class _GenCfg(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("n_tasks", ctypes.c_int32), ("n_opt", ctypes.c_int32),
+                ("opt_stride", ctypes.c_int32), ("horizon", ctypes.c_int32), ("u_lo_q16", ctypes.c_int32),
+                ("u_hi_q16", ctypes.c_int32), ("d_lo", ctypes.c_int32), ("release_mode", ctypes.c_int32)]
+
+
+EXPORTED = ("ic_sched_create", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
+            "ic_sched_get_info", "ic_gen_batch_device")
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB
+
+
+def load_library():
+    """Load libicsched.so; raise loudly if it was not built (no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise ImportError(f"{_LIB} is missing: run `python __graft_entry__.py build` "
+                              "(the solver has no CPU fallback)")
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.POINTER
+        lib.ic_sched_create.argtypes = [P(SchedConfig), P(ctypes.c_void_p)]
+        lib.ic_sched_solve_batch.argtypes = [ctypes.c_void_p, P(_In), P(_Out), ctypes.c_void_p]
+        lib.ic_sched_solve_batch_host.argtypes = [ctypes.c_void_p, P(_In), P(_Out), ctypes.c_void_p]
+        lib.ic_sched_destroy.argtypes = [ctypes.c_void_p]
+        lib.ic_sched_get_info.argtypes = [ctypes.c_void_p, P(SchedInfo)]
+        lib.ic_gen_batch_device.argtypes = [P(_GenCfg), ctypes.c_int64, ctypes.c_int64] + \
+            [ctypes.c_void_p] * 9
+        for f in EXPORTED:
+            getattr(lib, f).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _ptr(x):
+    """Device (torch) or host (numpy) buffer -> void*."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return ctypes.c_void_p(x.data_ptr()) if x.numel() else None
+    return ctypes.c_void_p(x.ctypes.data) if x.size else None
+
+
+def _n_instances(inputs) -> int:
+    tb = inputs["task_begin"]
+    return (tb.numel() if hasattr(tb, "numel") else tb.size) - 1
+
+
+def alloc_outputs(n_instances: int, n_tasks: int, device="cuda", pinned: bool = False, host=False) -> dict:
+    """Output buffers in the ABI layout: torch CUDA tensors, or host numpy / pinned torch."""
+    import torch
+    out = {}
+    for name, dt, kind in OUTPUT_FIELDS:
+        n = n_tasks if kind == "task" else n_instances
+        tdt = torch.from_numpy(np.zeros(0, dt)).dtype
+        if host:
+            out[name] = torch.empty(n, dtype=tdt, pin_memory=pinned)
+        else:
+            out[name] = torch.empty(n, dtype=tdt, device=device)
+    if host:
+        out["stats"] = torch.zeros(8, dtype=torch.int64, pin_memory=pinned)
+    else:
+        out["stats"] = torch.zeros(8, dtype=torch.int64, device=device)
+    return out
+
+
+class Scheduler:
+    """One ic_sched handle (bound to a device; one stream at a time)."""
+
+    def __init__(self, cfg: SchedConfig):
+        self._lib = load_library()
+        self.cfg = cfg
+        h = ctypes.c_void_p()
+        rc = self._lib.ic_sched_create(ctypes.byref(cfg), ctypes.byref(h))
+        if rc != IC_OK:
+            raise ICSchedError("ic_sched_create", rc)
+        self._h = h
+
+    def info(self) -> dict:
+        i = SchedInfo()
+        rc = self._lib.ic_sched_get_info(self._h, ctypes.byref(i))
+        if rc != IC_OK:
+            raise ICSchedError("ic_sched_get_info", rc)
+        return i.as_dict()
+
+    def _marshal(self, inputs, outputs):
+        i = _In(_n_instances(inputs), *[_ptr(inputs[n]) for n, _, _ in INPUT_FIELDS])
+        o = _Out(*[_ptr(outputs[n]) for n, _, _ in OUTPUT_FIELDS], _ptr(outputs.get("stats")))
+        return i, o
+
+    def solve_batch(self, inputs: dict, outputs: dict | None = None, stream=None) -> dict:
+        """ic_sched_solve_batch on CUDA tensors; asynchronous on `stream` (torch.cuda.Stream)."""
+        import torch
+        if outputs is None:
+            outputs = alloc_outputs(_n_instances(inputs), inputs["release"].numel(),
+                                    device=inputs["release"].device)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        i, o = self._marshal(inputs, outputs)
+        rc = self._lib.ic_sched_solve_batch(self._h, ctypes.byref(i), ctypes.byref(o),
+                                            ctypes.c_void_p(stream.cuda_stream))
+        if rc != IC_OK:
+            raise ICSchedError("ic_sched_solve_batch", rc)
+        return outputs
+
+    def solve_batch_host(self, inputs: dict, outputs: dict, stream=None) -> dict:
+        """ic_sched_solve_batch_host on host buffers (numpy or pinned torch); synchronous."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        i, o = self._marshal(inputs, outputs)
+        rc = self._lib.ic_sched_solve_batch_host(self._h, ctypes.byref(i), ctypes.byref(o),
+                                                 ctypes.c_void_p(stream.cuda_stream))
+        if rc != IC_OK:
+            raise ICSchedError("ic_sched_solve_batch_host", rc)
+        return outputs
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.ic_sched_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def gen_batch_device(seed, n_tasks, n_opt, opt_stride, horizon, u_lo_q16, u_hi_q16, d_lo, n_instances,
+                     id_offset=0, release_mode=0, device="cuda", stream=None) -> dict:
+    """ic_gen_batch_device: generate instances [id_offset, id_offset+n) on the GPU (ABI layout)."""
+    import torch
+    lib = load_library()
+    B, T = int(n_instances), int(n_instances) * int(n_tasks)
+    dev = torch.device(device)
+    t = {n: torch.empty((T, opt_stride) if k == "task_opt" else (B + 1 if k == "csr" else T),
+                        dtype=torch.from_numpy(np.zeros(0, dt)).dtype, device=dev)
+         for n, dt, k in INPUT_FIELDS}
+    g = _GenCfg(seed, n_tasks, n_opt, opt_stride, horizon, u_lo_q16, u_hi_q16, d_lo, release_mode)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    rc = lib.ic_gen_batch_device(ctypes.byref(g), id_offset, B, *[_ptr(t[n]) for n, _, _ in INPUT_FIELDS],
+                                 ctypes.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise ICSchedError("ic_gen_batch_device", rc)
+    return t

@@ -1,0 +1,308 @@
+// ic_sched.cu — the C ABI of include/ic_sched.h: handle, launch geometry,
+// workspace, and the host-buffer (end-to-end) entry point.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../../include/ic_sched.h"
+#include "ic_sched_kernel.cuh"
+
+using icsched::Params;
+
+namespace {
+
+constexpr int kMaxTasks = 4096;
+constexpr int kMaxOpt = 14;
+constexpr int kMaxHorizon = 32768;
+constexpr int kSmemLimit = 227 * 1024;
+
+typedef void (*KernelFn)(const Params);
+
+struct Variant {
+  int nt, cols;
+  bool single_buf;
+  KernelFn fn;
+};
+
+// Column capacity NT*COLS must cover max_horizon; the smallest fitting variant wins.
+const Variant kVariants[] = {
+    {32, 4, false, icsched::ic_dp_kernel<32, 4, false>},
+    {64, 8, false, icsched::ic_dp_kernel<64, 8, false>},
+    {128, 8, false, icsched::ic_dp_kernel<128, 8, false>},
+    {128, 16, false, icsched::ic_dp_kernel<128, 16, false>},
+    {256, 16, false, icsched::ic_dp_kernel<256, 16, false>},
+    {512, 16, false, icsched::ic_dp_kernel<512, 16, false>},
+    {512, 32, true, icsched::ic_dp_kernel<512, 32, true>},
+    {512, 64, true, icsched::ic_dp_kernel<512, 64, true>},
+};
+
+inline int align16(int x) { return (x + 15) & ~15; }
+
+struct Layout {
+  int bytes;
+  int off_rowbuf, off_dec, off_rowp, off_tR, off_info, off_key, off_tr, off_td, off_tS, off_chosen,
+      off_misc;
+  int kp, np2;
+};
+
+Layout make_layout(const ic_sched_config& c, const Variant& v, int pad, bool dec_smem) {
+  Layout L{};
+  const int cap = v.nt * v.cols;
+  const int nbuf = v.single_buf ? 1 : 2;
+  const int nq = (v.cols + 7) / 8;
+  L.kp = (c.max_opt_stages + 2) & ~1;  // options per task, even so int4 loads stay aligned
+  int np2 = 1;
+  while (np2 < c.max_tasks) np2 <<= 1;
+  L.np2 = np2 < 32 ? 32 : np2;
+  int o = 0;
+  L.off_rowbuf = o; o = align16(o + nbuf * (pad + cap) * 4);
+  L.off_dec = o;    if (dec_smem) o = align16(o + c.max_tasks * nq * v.nt * 4);
+  L.off_rowp = o;   o = align16(o + c.max_tasks * L.kp * 8);
+  L.off_tR = o;     o = align16(o + c.max_tasks * (c.max_opt_stages + 1) * 4);
+  L.off_info = o;   o = align16(o + c.max_tasks * 16);
+  L.off_key = o;    o = align16(o + L.np2 * 8);
+  L.off_tr = o;     o = align16(o + c.max_tasks * 4);
+  L.off_td = o;     o = align16(o + c.max_tasks * 4);
+  L.off_tS = o;     o = align16(o + c.max_tasks * 4);
+  L.off_chosen = o; o = align16(o + c.max_tasks * 4);
+  L.off_misc = o;   o = align16(o + 128);
+  L.bytes = o;
+  return L;
+}
+
+}  // namespace
+
+struct ic_sched {
+  ic_sched_config cfg;
+  const Variant* var;
+  Layout L;
+  int pad, dec_smem, sms, ctas_per_sm, grid;
+  uint32_t* dec_global;
+  int64_t dec_slab_words;
+  // staging for the host-buffer entry point
+  void* stage;
+  size_t stage_bytes;
+};
+
+extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
+  if (!cfg || !out) return IC_ERR_INVALID_ARG;
+  *out = nullptr;
+  const ic_sched_config c = *cfg;
+  if (c.drop_mode != IC_DROP_ALLOWED && c.drop_mode != IC_MANDATORY_ENFORCED) return IC_ERR_INVALID_ARG;
+  if (c.delta_micro == 0 && c.epsilon_micro == 0) return IC_ERR_INVALID_ARG;
+  if (c.max_tasks < 1 || c.max_opt_stages < 0 || c.max_horizon < 1) return IC_ERR_INVALID_ARG;
+  if (c.max_tasks > kMaxTasks || c.max_opt_stages > kMaxOpt || c.max_horizon > kMaxHorizon)
+    return IC_ERR_LIMIT;
+  if (cudaSetDevice(c.device) != cudaSuccess) return IC_ERR_CUDA;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device) != cudaSuccess)
+    return IC_ERR_CUDA;
+
+  const Variant* var = nullptr;
+  for (const Variant& v : kVariants)
+    if (v.nt * v.cols >= c.max_horizon) { var = &v; break; }
+  if (!var) return IC_ERR_LIMIT;
+  // NEG pad left of column 0: rows whose longest usable option is longer use the
+  // clamped general path, so the pad only trades shared memory for speed.
+  int pad = c.max_horizon < 1024 ? c.max_horizon : 1024;
+  pad = (pad + 31) & ~31;
+  if (var->single_buf && pad > 256) pad = 256;
+
+  // decisions in shared memory when they fit and leave room for >= 2 CTAs/SM
+  // (or always, via IC_SCHED_DEC=smem|global for experiments)
+  Layout Ls = make_layout(c, *var, pad, true);
+  Layout Lg = make_layout(c, *var, pad, false);
+  bool dec_smem = Ls.bytes <= kSmemLimit / 2;
+  const char* env = getenv("IC_SCHED_DEC");
+  if (env && !strcmp(env, "smem")) dec_smem = Ls.bytes <= kSmemLimit;
+  if (env && !strcmp(env, "global")) dec_smem = false;
+  const Layout L = dec_smem ? Ls : Lg;
+  if (L.bytes > kSmemLimit) return IC_ERR_LIMIT;
+
+  if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes) != cudaSuccess)
+    return IC_ERR_CUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->nt, L.bytes) != cudaSuccess)
+    return IC_ERR_CUDA;
+  if (per_sm < 1) return IC_ERR_LIMIT;
+
+  ic_sched* h = (ic_sched*)calloc(1, sizeof(ic_sched));
+  if (!h) return IC_ERR_OOM;
+  h->cfg = c;
+  h->var = var;
+  h->L = L;
+  h->pad = pad;
+  h->dec_smem = dec_smem ? 1 : 0;
+  h->sms = sms;
+  h->ctas_per_sm = per_sm;
+  h->grid = sms * per_sm;
+  if (!dec_smem) {
+    const int nq = (var->cols + 7) / 8;
+    h->dec_slab_words = (int64_t)c.max_tasks * nq * var->nt;
+    if (cudaMalloc(&h->dec_global, (size_t)h->dec_slab_words * 4 * h->grid) != cudaSuccess) {
+      free(h);
+      return IC_ERR_OOM;
+    }
+  }
+  *out = h;
+  return IC_OK;
+}
+
+extern "C" int ic_sched_destroy(ic_sched* h) {
+  if (!h) return IC_ERR_INVALID_ARG;
+  cudaSetDevice(h->cfg.device);
+  if (h->dec_global) cudaFree(h->dec_global);
+  if (h->stage) cudaFree(h->stage);
+  free(h);
+  return IC_OK;
+}
+
+extern "C" int ic_sched_get_info(const ic_sched* h, ic_sched_info* info) {
+  if (!h || !info) return IC_ERR_INVALID_ARG;
+  info->threads_per_cta = h->var->nt;
+  info->cols_per_thread = h->var->cols;
+  info->ctas_per_sm = h->ctas_per_sm;
+  info->grid = h->grid;
+  info->smem_bytes = h->L.bytes;
+  info->decisions_in_smem = h->dec_smem;
+  info->double_buffered = h->var->single_buf ? 0 : 1;
+  info->pad_cols = h->pad;
+  info->workspace_bytes = h->dec_smem ? 0 : h->dec_slab_words * 4 * h->grid;
+  return IC_OK;
+}
+
+static int check_io(const ic_batch_in* in, const ic_batch_out* out) {
+  if (!in || !out || in->n_instances < 0) return IC_ERR_INVALID_ARG;
+  if (in->n_instances == 0) return IC_OK;
+  if (!in->task_begin || !in->release || !in->deadline || !in->mand_wcet || !in->n_opt ||
+      !in->mand_conf)
+    return IC_ERR_INVALID_ARG;
+  if (!out->kept || !out->start || !out->finish || !out->q_total || !out->conf_micro ||
+      !out->conf_total || !out->makespan || !out->status)
+    return IC_ERR_INVALID_ARG;
+  return IC_OK;
+}
+
+extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch_out* out,
+                                    void* cuda_stream) {
+  if (!h) return IC_ERR_INVALID_ARG;
+  int rc = check_io(in, out);
+  if (rc != IC_OK) return rc;
+  if (h->cfg.max_opt_stages > 0 && in->n_instances > 0 && (!in->opt_wcet || !in->opt_gain))
+    return IC_ERR_INVALID_ARG;
+  if (in->n_instances == 0) return IC_OK;
+  if (cudaSetDevice(h->cfg.device) != cudaSuccess) return IC_ERR_CUDA;
+  Params p{};
+  p.B = in->n_instances;
+  p.task_begin = in->task_begin;
+  p.release = in->release;
+  p.deadline = in->deadline;
+  p.mand_wcet = in->mand_wcet;
+  p.n_opt = in->n_opt;
+  p.opt_wcet = in->opt_wcet;
+  p.mand_conf = in->mand_conf;
+  p.opt_gain = in->opt_gain;
+  p.kept = out->kept;
+  p.start = out->start;
+  p.finish = out->finish;
+  p.q_total = out->q_total;
+  p.conf_micro = out->conf_micro;
+  p.conf_total = out->conf_total;
+  p.makespan = out->makespan;
+  p.status = out->status;
+  p.stats = (unsigned long long*)out->stats;
+  p.drop_mode = h->cfg.drop_mode;
+  p.delta_micro = h->cfg.delta_micro;
+  p.eps_micro = h->cfg.epsilon_micro;
+  p.max_tasks = h->cfg.max_tasks;
+  p.smax = h->cfg.max_opt_stages;
+  p.H = h->cfg.max_horizon;
+  p.pad = h->pad;
+  p.nbuf = h->var->single_buf ? 1 : 2;
+  p.dec_smem = h->dec_smem;
+  p.kp = h->L.kp;
+  p.np2max = h->L.np2;
+  p.dec_global = h->dec_global;
+  p.dec_slab_words = h->dec_slab_words;
+  p.off_rowbuf = h->L.off_rowbuf;
+  p.off_dec = h->L.off_dec;
+  p.off_rowp = h->L.off_rowp;
+  p.off_tR = h->L.off_tR;
+  p.off_info = h->L.off_info;
+  p.off_key = h->L.off_key;
+  p.off_tr = h->L.off_tr;
+  p.off_td = h->L.off_td;
+  p.off_tS = h->L.off_tS;
+  p.off_chosen = h->L.off_chosen;
+  p.off_misc = h->L.off_misc;
+  int64_t grid = h->grid;
+  if (grid > in->n_instances) grid = in->n_instances;
+  h->var->fn<<<(unsigned)grid, h->var->nt, h->L.bytes, (cudaStream_t)cuda_stream>>>(p);
+  if (cudaGetLastError() != cudaSuccess) return IC_ERR_CUDA;
+  return IC_OK;
+}
+
+// Host-buffer entry point: H2D of the inputs, solve, D2H of the outputs, all on
+// `cuda_stream`, synchronised before returning.
+extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_batch_out* out,
+                                         void* cuda_stream) {
+  if (!h) return IC_ERR_INVALID_ARG;
+  int rc = check_io(in, out);
+  if (rc != IC_OK) return rc;
+  if (in->n_instances == 0) return IC_OK;
+  if (cudaSetDevice(h->cfg.device) != cudaSuccess) return IC_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int64_t B = in->n_instances;
+  int64_t first = 0, last = 0;
+  memcpy(&first, in->task_begin, 8);
+  memcpy(&last, in->task_begin + B, 8);
+  if (last < first) return IC_ERR_INVALID_ARG;
+  const int64_t T = last;  // rows [0, last) are addressed by the CSR offsets
+  const int64_t st = h->cfg.max_opt_stages;
+  // staging layout (8-byte aligned pieces)
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 15) & ~(size_t)15; return o; };
+  const size_t o_tb = take((B + 1) * 8), o_r = take(T * 4), o_d = take(T * 4), o_m = take(T * 4),
+               o_n = take(T), o_ow = take(T * st * 4), o_mc = take(T * 4), o_og = take(T * st * 4),
+               o_k = take(T), o_s = take(T * 4), o_f = take(T * 4), o_q = take(B * 8), o_c = take(B * 8),
+               o_ct = take(B * 8), o_ms = take(B * 4), o_st = take(B), o_stats = take(64);
+  if (off > h->stage_bytes) {
+    if (h->stage) cudaFree(h->stage);
+    h->stage = nullptr;
+    h->stage_bytes = 0;
+    if (cudaMalloc(&h->stage, off) != cudaSuccess) return IC_ERR_OOM;
+    h->stage_bytes = off;
+  }
+  char* g = (char*)h->stage;
+  auto h2d = [&](size_t o, const void* src, size_t bytes) {
+    return bytes == 0 || cudaMemcpyAsync(g + o, src, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  };
+  auto d2h = [&](void* dst, size_t o, size_t bytes) {
+    return bytes == 0 || cudaMemcpyAsync(dst, g + o, bytes, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  };
+  bool ok = h2d(o_tb, in->task_begin, (B + 1) * 8) && h2d(o_r, in->release, T * 4) &&
+            h2d(o_d, in->deadline, T * 4) && h2d(o_m, in->mand_wcet, T * 4) && h2d(o_n, in->n_opt, T) &&
+            h2d(o_mc, in->mand_conf, T * 4);
+  if (st > 0) ok = ok && h2d(o_ow, in->opt_wcet, T * st * 4) && h2d(o_og, in->opt_gain, T * st * 4);
+  if (out->stats) ok = ok && cudaMemsetAsync(g + o_stats, 0, 64, s) == cudaSuccess;
+  if (!ok) return IC_ERR_CUDA;
+  ic_batch_in din = {B, (const int64_t*)(g + o_tb), (const int32_t*)(g + o_r), (const int32_t*)(g + o_d),
+                     (const int32_t*)(g + o_m), (const uint8_t*)(g + o_n), (const int32_t*)(g + o_ow),
+                     (const uint32_t*)(g + o_mc), (const int32_t*)(g + o_og)};
+  ic_batch_out dout = {(int8_t*)(g + o_k), (int32_t*)(g + o_s), (int32_t*)(g + o_f), (int64_t*)(g + o_q),
+                       (int64_t*)(g + o_c), (double*)(g + o_ct), (int32_t*)(g + o_ms), (uint8_t*)(g + o_st),
+                       out->stats ? (int64_t*)(g + o_stats) : nullptr};
+  rc = ic_sched_solve_batch(h, &din, &dout, cuda_stream);
+  if (rc != IC_OK) return rc;
+  ok = d2h(out->kept, o_k, T) && d2h(out->start, o_s, T * 4) && d2h(out->finish, o_f, T * 4) &&
+       d2h(out->q_total, o_q, B * 8) && d2h(out->conf_micro, o_c, B * 8) &&
+       d2h(out->conf_total, o_ct, B * 8) && d2h(out->makespan, o_ms, B * 4) && d2h(out->status, o_st, B);
+  int64_t stats_dev[8];
+  if (out->stats) ok = ok && d2h(stats_dev, o_stats, 64);
+  if (!ok) return IC_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return IC_ERR_CUDA;
+  if (out->stats)
+    for (int i = 0; i < 8; ++i) out->stats[i] += stats_dev[i];
+  return IC_OK;
+}

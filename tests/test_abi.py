@@ -1,0 +1,66 @@
+"""The C-ABI library loads and exports every symbol include/*.h declares (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2011_01112_b200 as pkg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared(header):
+    txt = open(os.path.join(ROOT, "include", header)).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return set(re.findall(r"^\s*int\s+(ic_\w+)\s*\(", txt, flags=re.M))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = pkg.load_library()
+    declared = _declared("ic_sched.h") | (_declared("ic_gen.h") - {"ic_gen_batch_host"})
+    assert declared == set(pkg.abi.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_host_generator_symbol():
+    import gen
+    lib = gen._load()
+    assert hasattr(lib, "ic_gen_batch_host")
+
+
+def test_invalid_configs_rejected_before_cuda():
+    lib = pkg.load_library()
+    h = ctypes.c_void_p()
+    bad = [pkg.SchedConfig(delta_micro=0, epsilon_micro=0),
+           pkg.SchedConfig(drop_mode=7),
+           pkg.SchedConfig(max_tasks=0)]
+    for c in bad:
+        assert lib.ic_sched_create(ctypes.byref(c), ctypes.byref(h)) == pkg.IC_ERR_INVALID_ARG
+    for c in (pkg.SchedConfig(max_tasks=5000), pkg.SchedConfig(max_opt_stages=15),
+              pkg.SchedConfig(max_horizon=40000)):
+        assert lib.ic_sched_create(ctypes.byref(c), ctypes.byref(h)) == pkg.IC_ERR_LIMIT
+    assert lib.ic_sched_create(None, ctypes.byref(h)) == pkg.IC_ERR_INVALID_ARG
+    assert lib.ic_sched_solve_batch(None, None, None, None) == pkg.IC_ERR_INVALID_ARG
+    assert lib.ic_sched_destroy(None) == pkg.IC_ERR_INVALID_ARG
+
+
+def test_no_cpu_fallback_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(pkg.ICSchedError) as e:
+        pkg.Scheduler(pkg.SchedConfig())
+    assert e.value.rc == pkg.IC_ERR_CUDA
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path must never route through oracle/ (task brief ③)."""
+    pdir = os.path.join(ROOT, "paper_2011_01112_b200")
+    for dirpath, _, files in os.walk(pdir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                for pat in ("import oracle", "from oracle", "liboracle", "ic_oracle"):
+                    assert pat not in src, (f, pat)

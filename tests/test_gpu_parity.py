@@ -1,0 +1,209 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Decisions, integer times, Q, makespan and status must match bit for bit;
+total confidence to 1e-6 relative (north_star).  Inputs are seeded: the
+paper-shaped generator (gen/) and small adversarial instances.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from oracle import OracleConfig, BRUTE, PAPER, TIME
+from tests._instances import batch_from_tasks, batch_from_many
+from tests.gpu_util import assert_parity, gpu_solve, stats_from
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("delta,eps", [(100_000, 0), (30_000, 0), (0, 250_000), (0, 100_000)])
+def test_tiny_random_vs_brute_force(mode, delta, eps):
+    rng = np.random.default_rng(100 + mode + delta + eps)
+    batch = gen.tiny_random(rng, 20000, max_tasks=5, max_opt=3, horizon=24)
+    cfg = OracleConfig(drop_mode=mode, delta_micro=delta, epsilon_micro=eps, max_tasks=5, max_horizon=24)
+    ref = oracle.solve(batch, cfg, BRUTE)
+    got = gpu_solve(batch, max_tasks=5, max_opt=3, max_horizon=24, drop_mode=mode, delta=delta, eps=eps)
+    assert_parity(got, ref, f"tiny mode={mode} delta={delta} eps={eps}")
+
+
+@pytest.mark.parametrize("name,n,algo", [("C1", 20000, PAPER), ("C2", 3000, PAPER), ("C3", 300, TIME),
+                                         ("C4", 3, TIME)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_paper_shaped_configs(name, n, algo, mode):
+    cw = gen.CONFIGS[name]
+    batch = gen.generate(cw, n)
+    ocfg = OracleConfig(drop_mode=mode, epsilon_micro=cw.epsilon_micro, max_tasks=cw.n_tasks,
+                        max_horizon=cw.horizon)
+    ref = oracle.solve(batch, ocfg, algo)
+    got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
+                    eps=cw.epsilon_micro)
+    assert_parity(got, ref, f"{name} mode={mode}")
+    assert (oracle.check(batch, got, ocfg) == 0).all()
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_paper_delta_point_one(name):
+    """The paper's experimental default Delta = 0.1."""
+    cw = gen.CONFIGS[name]
+    batch = gen.generate(cw, 400 if name == "C2" else 100)
+    ref = oracle.solve(batch, OracleConfig(delta_micro=100_000, max_tasks=cw.n_tasks, max_horizon=cw.horizon),
+                       PAPER)
+    got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, delta=100_000)
+    assert_parity(got, ref, name)
+
+
+def test_releases_and_variable_stages():
+    """Releases (frames mode), ragged S_i, non-monotone curves at C2 scale."""
+    rng = np.random.default_rng(5)
+    parts = []
+    for _ in range(300):
+        N = int(rng.integers(1, 40))
+        ts = []
+        for _ in range(N):
+            S = int(rng.integers(0, 5))
+            lv = rng.integers(0, 101, S + 1) * 10_000
+            if rng.random() < 0.5:
+                lv = np.sort(lv)
+            ts.append(dict(r=int(rng.integers(0, 300)) if rng.random() < 0.5 else 0,
+                           d=int(rng.integers(-5, 1024)), m=int(rng.integers(1, 40)),
+                           w=[int(x) for x in rng.integers(1, 40, S)], a0=int(lv[0]),
+                           g=[int(x) for x in np.diff(lv)]))
+        parts.append(ts)
+    batch = batch_from_many(parts, 4)
+    for mode in (0, 1):
+        ocfg = OracleConfig(drop_mode=mode, epsilon_micro=100_000, max_tasks=40, max_horizon=1024)
+        ref = oracle.solve(batch, ocfg, TIME)
+        got = gpu_solve(batch, max_tasks=40, max_opt=4, max_horizon=1024, drop_mode=mode)
+        assert_parity(got, ref, f"releases mode={mode}")
+
+
+def test_general_path_long_tasks():
+    """Options longer than the NEG pad take the clamped general path."""
+    rng = np.random.default_rng(6)
+    parts = []
+    for _ in range(60):
+        N = int(rng.integers(1, 12))
+        ts = []
+        for _ in range(N):
+            S = int(rng.integers(0, 4))
+            lv = np.sort(rng.integers(0, 101, S + 1)) * 10_000
+            ts.append(dict(r=0, d=int(rng.integers(500, 4096)), m=int(rng.integers(1, 1500)),
+                           w=[int(x) for x in rng.integers(1, 900, S)], a0=int(lv[0]),
+                           g=[int(x) for x in np.diff(lv)]))
+        parts.append(ts)
+    batch = batch_from_many(parts, 3)
+    ref = oracle.solve(batch, OracleConfig(delta_micro=20_000, max_tasks=16, max_horizon=4096), TIME)
+    got = gpu_solve(batch, max_tasks=16, max_opt=3, max_horizon=4096, delta=20_000)
+    assert_parity(got, ref, "general path")
+
+
+def test_many_tasks_block_sort():
+    """N > 32 uses the shared-memory bitonic sort; ragged N; equal deadlines."""
+    rng = np.random.default_rng(7)
+    parts = []
+    for _ in range(100):
+        N = int(rng.integers(0, 300))
+        ts = []
+        dl = rng.integers(0, 200, N)
+        if rng.random() < 0.5:
+            dl = dl // 20 * 20  # many equal deadlines
+        for i in range(N):
+            S = int(rng.integers(0, 3))
+            lv = np.sort(rng.integers(0, 101, S + 1)) * 10_000
+            ts.append(dict(r=0, d=int(dl[i]), m=int(rng.integers(1, 4)),
+                           w=[int(x) for x in rng.integers(1, 4, S)], a0=int(lv[0]),
+                           g=[int(x) for x in np.diff(lv)]))
+        parts.append(ts)
+    batch = batch_from_many(parts, 2)
+    ref = oracle.solve(batch, OracleConfig(epsilon_micro=100_000, max_tasks=300, max_horizon=256), TIME)
+    got = gpu_solve(batch, max_tasks=300, max_opt=2, max_horizon=256)
+    assert_parity(got, ref, "block sort")
+
+
+def test_bad_input_and_empty():
+    base = dict(r=0, d=5, m=1, w=[1], a0=300_000, g=[100_000])
+    lists = [[], [base], [dict(base, m=0)], [dict(base, w=[0])], [dict(base, r=-1)], [dict(base, d=64)],
+             [dict(base, a0=1_000_001)], [dict(base, g=[800_000])], [base] * 9, [dict(base, g=[-200_000])]]
+    batch = batch_from_many(lists, 1)
+    ref = oracle.solve(batch, OracleConfig(delta_micro=100_000, max_tasks=8, max_horizon=64), PAPER)
+    got = gpu_solve(batch, max_tasks=8, max_opt=1, max_horizon=64, delta=100_000)
+    assert_parity(got, ref, "bad input")
+    assert list(got["status"]) == [0, 0, 2, 2, 2, 2, 2, 2, 2, 0]
+
+
+def test_limit_status():
+    """16 * sum max q + 16 N >= 2^30 cannot be packed: IC_INST_LIMIT, everything dropped."""
+    t = dict(r=0, d=10, m=1, w=[], g=[], a0=1_000_000)
+    batch = batch_from_tasks([t] * 70)  # Delta = 1 -> q = 1e6 per task
+    got = gpu_solve(batch, max_tasks=70, max_opt=0, max_horizon=64, delta=1)
+    assert got["status"][0] == 3 and (got["kept"] == -1).all()
+
+
+def test_host_entry_point_and_stats():
+    cw = gen.CONFIGS["C2"]
+    batch = gen.generate(cw, 500)
+    a = gpu_solve(batch, max_tasks=32, max_opt=4, max_horizon=1024)
+    b = gpu_solve(batch, max_tasks=32, max_opt=4, max_horizon=1024, host=True)
+    assert_parity(a, b, "host vs device")
+    np.testing.assert_array_equal(a["stats"], stats_from(a, batch))
+    np.testing.assert_array_equal(b["stats"], stats_from(a, batch))
+
+
+def test_device_generator_matches_host():
+    import paper_2011_01112_b200 as pkg
+    for name in ("C1", "C2", "C3"):
+        cw = gen.CONFIGS[name]
+        host = gen.generate(cw, 257, id_offset=1000)
+        gc = cw.gen_config()
+        dev = pkg.gen_batch_device(gc.seed, gc.n_tasks, gc.n_opt, gc.opt_stride, gc.horizon, gc.u_lo_q16,
+                                   gc.u_hi_q16, gc.d_lo, 257, id_offset=1000)
+        torch.cuda.synchronize()
+        for f, _, _ in pkg.INPUT_FIELDS:
+            np.testing.assert_array_equal(dev[f].cpu().numpy(), getattr(host, f), err_msg=f)
+
+
+def test_decisions_in_global_memory(monkeypatch):
+    """The global-slab decision store gives identical results."""
+    monkeypatch.setenv("IC_SCHED_DEC", "global")
+    cw = gen.CONFIGS["C2"]
+    batch = gen.generate(cw, 300)
+    ref = oracle.solve(batch, OracleConfig(epsilon_micro=100_000, max_tasks=32, max_horizon=1024), PAPER)
+    got = gpu_solve(batch, max_tasks=32, max_opt=4, max_horizon=1024)
+    assert got["_info"]["decisions_in_smem"] == 0
+    assert_parity(got, ref, "global decisions")
+
+
+@pytest.mark.parametrize("name,sample", [("C2", 97), ("C3", 2003)])
+def test_full_size_sampled(name, sample):
+    """BASELINE.json full sizes in the bench launch configuration (device-generated inputs);
+    a deterministic sample is checked element by element against the oracle, every instance by
+    the invariant checker (C2) and the stats vector against the outputs."""
+    import paper_2011_01112_b200 as pkg
+    cw = gen.CONFIGS[name]
+    gc = cw.gen_config()
+    B = cw.n_instances
+    dev = pkg.gen_batch_device(gc.seed, gc.n_tasks, gc.n_opt, gc.opt_stride, gc.horizon, gc.u_lo_q16,
+                               gc.u_hi_q16, gc.d_lo, B)
+    sc = pkg.SchedConfig(max_tasks=cw.n_tasks, max_opt_stages=cw.n_opt, max_horizon=cw.horizon,
+                         epsilon_micro=cw.epsilon_micro)
+    with pkg.Scheduler(sc) as s:
+        out = s.solve_batch(dev)
+        torch.cuda.synchronize()
+    got = {k: v.cpu().numpy() for k, v in out.items()}
+    N = cw.n_tasks
+    idx = np.arange(0, B, sample)
+    parts = [gen.generate(cw, 1, id_offset=int(b)) for b in idx]
+    sub = gen.concat(parts, cw.n_opt)
+    ocfg = OracleConfig(epsilon_micro=cw.epsilon_micro, max_tasks=N, max_horizon=cw.horizon)
+    ref = oracle.solve(sub, ocfg, TIME)
+    tmask = (np.arange(B * N).reshape(B, N)[idx]).ravel()
+    picked = {k: (got[k][tmask] if k in ("kept", "start", "finish") else got[k][idx])
+              for k in ("kept", "start", "finish", "q_total", "conf_micro", "conf_total", "makespan", "status")}
+    assert_parity(picked, ref, f"{name} sampled")
+    assert got["stats"][0] == B
+    assert got["stats"][6] == got["conf_micro"].sum() and got["stats"][7] == got["q_total"].sum()
