@@ -47,11 +47,18 @@ def _sms():
 
 
 def algorithmic_evals(inputs, n_tasks, opt_stride, chunk=65536):
-    """W = sum_i [(T+1) + sum_k #{t <= d_i : t - C_i(k) >= r_i}] per instance,
-    T = max(0, max_i d_i).  Measurement only (torch ops on the generated inputs)."""
+    """Algorithmic option evaluations of a batch (measurement only; torch ops on the inputs).
+
+    Returns (W_active, W_survey):
+      W_survey = sum_i [(T+1) + sum_k #{t <= d_i : t - C_i(k) >= r_i}], T = max(0, max_i d_i)
+                 (SURVEY.md §8(d): every row evaluates every column of the time axis);
+      W_active = sum_i [(d_i + 1)^+ + sum_k #{t <= d_i : t - C_i(k) >= r_i}]
+                 (this kernel: columns t > d_i of row i share one value, DESIGN.md §5,
+                 so only the active columns t <= d_i are evaluated).
+    Each evaluation reads one 4-byte DP cell from shared memory."""
     import torch
     B = inputs["task_begin"].numel() - 1
-    total = 0
+    wa = ws = 0
     for lo in range(0, B, chunk):
         hi = min(B, lo + chunk)
         sl = slice(lo * n_tasks, hi * n_tasks)
@@ -64,10 +71,11 @@ def algorithmic_evals(inputs, n_tasks, opt_stride, chunk=65536):
         valid = k <= S[:, None]
         d = inputs["deadline"][sl].long()
         r = inputs["release"][sl].long()
-        cnt = torch.clamp(d[:, None] - r[:, None] - C + 1, min=0) * valid
+        opts = int((torch.clamp(d[:, None] - r[:, None] - C + 1, min=0) * valid).sum())
         T = torch.clamp(d.view(-1, n_tasks).max(1).values, min=0)
-        total += int(((T + 1) * n_tasks).sum() + cnt.sum())
-    return total
+        ws += int(((T + 1) * n_tasks).sum()) + opts
+        wa += int(torch.clamp(d + 1, min=0).sum()) + opts
+    return wa, ws
 
 
 class ClockSampler:
@@ -176,7 +184,7 @@ def run_reference(args, cw, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: >= 1 s of work)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--instances", type=int, default=0, help="override instances per GPU")
@@ -194,19 +202,21 @@ def main():
     cw = gen.CONFIGS[args.config]
 
     if args.impl == "reference":
+        args.steps = args.steps or 3
         run_reference(args, cw, rank, world)
         return
 
     import torch
     import torch.distributed as dist
     import paper_2011_01112_b200 as pkg
+    from paper_2011_01112_b200.multigpu import reduce_stats, weak_shard
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n_inst = args.instances or (cw.u_blocks and cw.n_instances // max(world, 1)) or cw.n_instances
-    id0 = rank * n_inst
+    id0 = weak_shard(n_inst, rank)[0]
     stream = torch.cuda.Stream(dev)
 
     # ---- inputs resident in HBM: this rank's global-id shard, generated on device
@@ -231,7 +241,7 @@ def main():
     stream.synchronize()
     T = n_inst * cw.n_tasks
     in_bytes = sum(v.numel() * v.element_size() for v in inputs.values())
-    W = algorithmic_evals(inputs, cw.n_tasks, cw.n_opt)
+    W, W_survey = algorithmic_evals(inputs, cw.n_tasks, cw.n_opt)
 
     sc = pkg.SchedConfig(device=local, max_tasks=cw.n_tasks, max_opt_stages=cw.n_opt, max_horizon=cw.horizon,
                          delta_micro=args.delta_micro, epsilon_micro=cw.epsilon_micro)
@@ -243,13 +253,24 @@ def main():
     def step():
         out["stats"].zero_()
         sched.solve_batch(inputs, out, stream)
-        if world > 1:
-            dist.all_reduce(out["stats"])
+        reduce_stats(out["stats"])
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step()
     stream.synchronize()
+    if args.steps is None:  # default: enough steps for >= 1 s of timed work (clock samples)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        k = max(10, int(1000.0 / max(e0.elapsed_time(e1), 1e-3)) + 1)
+        kt = torch.tensor([k], device=dev)
+        if world > 1:
+            dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+        args.steps = int(kt.item())
     if world > 1:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -262,8 +283,7 @@ def main():
             ev[i][0].record(stream)
             sched.solve_batch(inputs, out, stream)
             ev[i][1].record(stream)
-            if world > 1:
-                dist.all_reduce(out["stats"])
+            reduce_stats(out["stats"])
         t_end.record(stream)
         stream.synchronize()
     torch.cuda.synchronize(dev)
@@ -326,7 +346,10 @@ def main():
                          "frac": achieved / peak_gbs, "traffic": traffic,
                          "peak_basis": f"128 B/clk/SM LDS x {sms} SMs x {fmax:.0f} MHz (guide-derived; no "
                                        "measured smem peak in MEASURED_PEAKS.json)",
-                         "evals_per_instance": W / n_inst, "kernel_ms": kern_ms},
+                         "evals_per_instance": W / n_inst, "kernel_ms": kern_ms,
+                         "work": "W_active evals x 4 B (DESIGN.md §5)",
+                         "survey_evals_per_instance": W_survey / n_inst,
+                         "achieved_at_survey_W": W_survey * BYTES_PER_EVAL / (kern_ms / 1e3) / 1e9},
             "gpu_launches": args.steps,
             "clocks": clk_s,
             "kernel": info,

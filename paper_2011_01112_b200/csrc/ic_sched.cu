@@ -17,56 +17,59 @@ constexpr int kMaxOpt = 14;
 constexpr int kMaxHorizon = 32768;
 constexpr int kSmemLimit = 227 * 1024;
 
-typedef void (*KernelFn)(const Params);
+using icsched::KernelFn;
 
-struct Variant {
-  int nt, cols;
-  bool single_buf;
-  KernelFn fn;
-};
-
-// Column capacity NT*COLS must cover max_horizon; the smallest fitting variant wins.
-const Variant kVariants[] = {
-    {32, 4, false, icsched::ic_dp_kernel<32, 4, false>},
-    {64, 8, false, icsched::ic_dp_kernel<64, 8, false>},
-    {128, 8, false, icsched::ic_dp_kernel<128, 8, false>},
-    {128, 16, false, icsched::ic_dp_kernel<128, 16, false>},
-    {256, 16, false, icsched::ic_dp_kernel<256, 16, false>},
-    {512, 16, false, icsched::ic_dp_kernel<512, 16, false>},
-    {512, 32, true, icsched::ic_dp_kernel<512, 32, true>},
-    {512, 64, true, icsched::ic_dp_kernel<512, 64, true>},
-};
+KernelFn kernel_for(int nw, bool sb, bool drop) {
+  switch (nw) {
+    case 1: return icsched::kernel_nw1(sb, drop);
+    case 2: return icsched::kernel_nw2(sb, drop);
+    case 4: return icsched::kernel_nw4(sb, drop);
+    case 8: return icsched::kernel_nw8(sb, drop);
+    case 16: return icsched::kernel_nw16(sb, drop);
+    default: return nullptr;
+  }
+}
 
 inline int align16(int x) { return (x + 15) & ~15; }
 
 struct Layout {
-  int bytes;
-  int off_rowbuf, off_dec, off_rowp, off_tR, off_info, off_key, off_tr, off_td, off_tS, off_chosen,
-      off_misc;
-  int kp, np2;
+  int bytes, nq, kp, r1, np2, pad, rs, nbuf;
+  int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
+      off_sS, off_key;
+  int nslots;
 };
 
-Layout make_layout(const ic_sched_config& c, const Variant& v, int pad, bool dec_smem) {
+Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_smem, int nslots = 2) {
   Layout L{};
-  const int cap = v.nt * v.cols;
-  const int nbuf = v.single_buf ? 1 : 2;
-  const int nq = (v.cols + 7) / 8;
-  L.kp = (c.max_opt_stages + 2) & ~1;  // options per task, even so int4 loads stay aligned
+  const int nt = 32 * nw;
+  const int cols = (c.max_horizon + nt - 1) / nt;
+  const int cap = nt * cols;
+  const int mt = c.max_tasks;
+  L.nq = (cols + 7) / 8;
+  L.kp = (c.max_opt_stages + 2) & ~1;  // (C, key) pairs per row, even for int4 loads
+  L.r1 = c.max_opt_stages + 1;
   int np2 = 1;
-  while (np2 < c.max_tasks) np2 <<= 1;
+  while (np2 < mt) np2 <<= 1;
   L.np2 = np2 < 32 ? 32 : np2;
+  L.pad = pad;
+  L.rs = (pad + cap + 3) & ~3;
+  L.nbuf = sb ? 1 : 2;
+  L.nslots = nslots;
+  const int ns = nslots;
   int o = 0;
-  L.off_rowbuf = o; o = align16(o + nbuf * (pad + cap) * 4);
-  L.off_dec = o;    if (dec_smem) o = align16(o + c.max_tasks * nq * v.nt * 4);
-  L.off_rowp = o;   o = align16(o + c.max_tasks * L.kp * 8);
-  L.off_tR = o;     o = align16(o + c.max_tasks * (c.max_opt_stages + 1) * 4);
-  L.off_info = o;   o = align16(o + c.max_tasks * 16);
+  L.off_rowbuf = o; o = align16(o + L.nbuf * L.rs * 4);
+  L.off_dec = o;    if (dec_smem) o = align16(o + mt * L.nq * nt * 4);
+  L.off_rowp = o;   o = align16(o + ns * mt * L.kp * 8);
+  L.off_info = o;   o = align16(o + ns * mt * 16);
+  L.off_tR = o;     o = align16(o + ns * mt * L.r1 * 4);
+  L.off_task = o;   o = align16(o + ns * mt * 4);
+  L.off_tail = o;   o = align16(o + ns * mt * 4);
+  L.off_misc = o;   o = align16(o + 2 * 16 * 8);
+  L.off_chosen = o; o = align16(o + mt * 4);
+  L.off_sd = o;     o = align16(o + mt * 4);
+  L.off_sr = o;     o = align16(o + mt * 4);
+  L.off_sS = o;     o = align16(o + mt * 4);
   L.off_key = o;    o = align16(o + L.np2 * 8);
-  L.off_tr = o;     o = align16(o + c.max_tasks * 4);
-  L.off_td = o;     o = align16(o + c.max_tasks * 4);
-  L.off_tS = o;     o = align16(o + c.max_tasks * 4);
-  L.off_chosen = o; o = align16(o + c.max_tasks * 4);
-  L.off_misc = o;   o = align16(o + 128);
   L.bytes = o;
   return L;
 }
@@ -75,15 +78,21 @@ Layout make_layout(const ic_sched_config& c, const Variant& v, int pad, bool dec
 
 struct ic_sched {
   ic_sched_config cfg;
-  const Variant* var;
+  int nw;
+  bool sb;
+  KernelFn fn;
   Layout L;
-  int pad, dec_smem, sms, ctas_per_sm, grid;
+  int dec_smem, sms, ctas_per_sm, grid;
   uint32_t* dec_global;
   int64_t dec_slab_words;
-  // staging for the host-buffer entry point
   void* stage;
   size_t stage_bytes;
 };
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
 
 extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   if (!cfg || !out) return IC_ERR_INVALID_ARG;
@@ -98,48 +107,64 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device) != cudaSuccess)
     return IC_ERR_CUDA;
+  const bool drop = c.drop_mode == IC_DROP_ALLOWED;
 
-  const Variant* var = nullptr;
-  for (const Variant& v : kVariants)
-    if (v.nt * v.cols >= c.max_horizon) { var = &v; break; }
-  if (!var) return IC_ERR_LIMIT;
-  // NEG pad left of column 0: rows whose longest usable option is longer use the
-  // clamped general path, so the pad only trades shared memory for speed.
-  int pad = c.max_horizon < 1024 ? c.max_horizon : 1024;
+  // DP warps per instance: about 32 column groups per thread (IC_SCHED_NW overrides).
+  int nw = 1;
+  while (nw < 16 && 32 * nw * 32 < c.max_horizon) nw *= 2;
+  nw = env_int("IC_SCHED_NW", nw);
+  if (nw != 1 && nw != 2 && nw != 4 && nw != 8 && nw != 16) return IC_ERR_INVALID_ARG;
+  // NEG pad left of column 0: rows whose longest usable option reaches further use
+  // the masked general path, so the pad only trades shared memory for speed.
+  int pad = c.max_horizon < 256 ? c.max_horizon : 256;
+  pad = env_int("IC_SCHED_PAD", pad);
   pad = (pad + 31) & ~31;
-  if (var->single_buf && pad > 256) pad = 256;
 
-  // decisions in shared memory when they fit and leave room for >= 2 CTAs/SM
-  // (or always, via IC_SCHED_DEC=smem|global for experiments)
-  Layout Ls = make_layout(c, *var, pad, true);
-  Layout Lg = make_layout(c, *var, pad, false);
+  bool sb = env_int("IC_SCHED_SB", 0) != 0;  // in-place rows (tests force it at small H)
+  if (sb && nw < 8) nw = 8;
+  Layout Lg = make_layout(c, nw, sb, pad, false);
+  if (!sb && Lg.bytes > kSmemLimit) {
+    sb = true;
+    if (nw < 8) nw = 8;
+    Lg = make_layout(c, nw, true, pad, false);
+  }
+  int nslots = env_int("IC_SCHED_SLOTS", 2) == 1 ? 1 : 2;
+  if (Lg.bytes > kSmemLimit || nslots == 1) {  // serialise setup and sweep to fit large task sets
+    nslots = 1;
+    Lg = make_layout(c, nw, sb, pad, false, 1);
+  }
+  if (Lg.bytes > kSmemLimit) return IC_ERR_LIMIT;
+  Layout Ls = make_layout(c, nw, sb, pad, true, nslots);
+  // decisions in shared memory when that still leaves >= 2 CTAs per SM (IC_SCHED_DEC overrides)
   bool dec_smem = Ls.bytes <= kSmemLimit / 2;
   const char* env = getenv("IC_SCHED_DEC");
   if (env && !strcmp(env, "smem")) dec_smem = Ls.bytes <= kSmemLimit;
   if (env && !strcmp(env, "global")) dec_smem = false;
   const Layout L = dec_smem ? Ls : Lg;
-  if (L.bytes > kSmemLimit) return IC_ERR_LIMIT;
 
-  if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes) != cudaSuccess)
+  KernelFn fn = kernel_for(nw, sb, drop);
+  if (!fn) return IC_ERR_LIMIT;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes) != cudaSuccess)
     return IC_ERR_CUDA;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->nt, L.bytes) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (nw + 1), L.bytes) != cudaSuccess)
     return IC_ERR_CUDA;
   if (per_sm < 1) return IC_ERR_LIMIT;
+  per_sm = env_int("IC_SCHED_CTAS", per_sm) < per_sm ? env_int("IC_SCHED_CTAS", per_sm) : per_sm;
 
   ic_sched* h = (ic_sched*)calloc(1, sizeof(ic_sched));
   if (!h) return IC_ERR_OOM;
   h->cfg = c;
-  h->var = var;
+  h->nw = nw;
+  h->sb = sb;
+  h->fn = fn;
   h->L = L;
-  h->pad = pad;
   h->dec_smem = dec_smem ? 1 : 0;
   h->sms = sms;
   h->ctas_per_sm = per_sm;
   h->grid = sms * per_sm;
   if (!dec_smem) {
-    const int nq = (var->cols + 7) / 8;
-    h->dec_slab_words = (int64_t)c.max_tasks * nq * var->nt;
+    h->dec_slab_words = (int64_t)c.max_tasks * L.nq * 32 * nw;
     if (cudaMalloc(&h->dec_global, (size_t)h->dec_slab_words * 4 * h->grid) != cudaSuccess) {
       free(h);
       return IC_ERR_OOM;
@@ -160,14 +185,14 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
 
 extern "C" int ic_sched_get_info(const ic_sched* h, ic_sched_info* info) {
   if (!h || !info) return IC_ERR_INVALID_ARG;
-  info->threads_per_cta = h->var->nt;
-  info->cols_per_thread = h->var->cols;
+  info->threads_per_cta = 32 * (h->nw + 1);
+  info->cols_per_thread = (h->cfg.max_horizon + 32 * h->nw - 1) / (32 * h->nw);
   info->ctas_per_sm = h->ctas_per_sm;
   info->grid = h->grid;
   info->smem_bytes = h->L.bytes;
   info->decisions_in_smem = h->dec_smem;
-  info->double_buffered = h->var->single_buf ? 0 : 1;
-  info->pad_cols = h->pad;
+  info->double_buffered = h->sb ? 0 : 1;
+  info->pad_cols = h->L.pad;
   info->workspace_bytes = h->dec_smem ? 0 : h->dec_slab_words * 4 * h->grid;
   return IC_OK;
 }
@@ -212,33 +237,38 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   p.makespan = out->makespan;
   p.status = out->status;
   p.stats = (unsigned long long*)out->stats;
-  p.drop_mode = h->cfg.drop_mode;
   p.delta_micro = h->cfg.delta_micro;
   p.eps_micro = h->cfg.epsilon_micro;
   p.max_tasks = h->cfg.max_tasks;
   p.smax = h->cfg.max_opt_stages;
   p.H = h->cfg.max_horizon;
-  p.pad = h->pad;
-  p.nbuf = h->var->single_buf ? 1 : 2;
+  const Layout& L = h->L;
+  p.pad = L.pad;
+  p.nq = L.nq;
+  p.kp = L.kp;
+  p.r1 = L.r1;
+  p.np2 = L.np2;
   p.dec_smem = h->dec_smem;
-  p.kp = h->L.kp;
-  p.np2max = h->L.np2;
   p.dec_global = h->dec_global;
   p.dec_slab_words = h->dec_slab_words;
-  p.off_rowbuf = h->L.off_rowbuf;
-  p.off_dec = h->L.off_dec;
-  p.off_rowp = h->L.off_rowp;
-  p.off_tR = h->L.off_tR;
-  p.off_info = h->L.off_info;
-  p.off_key = h->L.off_key;
-  p.off_tr = h->L.off_tr;
-  p.off_td = h->L.off_td;
-  p.off_tS = h->L.off_tS;
-  p.off_chosen = h->L.off_chosen;
-  p.off_misc = h->L.off_misc;
+  p.off_rowbuf = L.off_rowbuf;
+  p.off_dec = L.off_dec;
+  p.off_rowp = L.off_rowp;
+  p.off_info = L.off_info;
+  p.off_tR = L.off_tR;
+  p.off_task = L.off_task;
+  p.off_tail = L.off_tail;
+  p.off_misc = L.off_misc;
+  p.off_chosen = L.off_chosen;
+  p.off_sd = L.off_sd;
+  p.off_sr = L.off_sr;
+  p.off_sS = L.off_sS;
+  p.off_key = L.off_key;
+  p.rowbuf_stride = L.rs;
+  p.nslots = L.nslots;
   int64_t grid = h->grid;
   if (grid > in->n_instances) grid = in->n_instances;
-  h->var->fn<<<(unsigned)grid, h->var->nt, h->L.bytes, (cudaStream_t)cuda_stream>>>(p);
+  h->fn<<<(unsigned)grid, 32 * (h->nw + 1), h->L.bytes, (cudaStream_t)cuda_stream>>>(p);
   if (cudaGetLastError() != cudaSuccess) return IC_ERR_CUDA;
   return IC_OK;
 }

@@ -1,40 +1,43 @@
 // ic_sched_kernel.cuh — sm_100a kernel for the batched depth assignment.
 //
-// One CTA solves one instance at a time (persistent grid-stride loop over
-// instances).  Per instance:
-//   a1  task descriptors: coalesced loads, one thread per task
-//   a2  prefix sums C_i(k), R_i(k), Delta (P:L78 / Thm 1),
-//       q = R div Delta, packed option keys (q << 4) | (15 - code)
-//   a3  EDF order by (d, r, idx): warp-shuffle bitonic sort for
-//       N <= 32, shared-memory bitonic otherwise
-//   a4  the DP sweep — the time-indexed dual of Eqs. 1-2:
-//         G_i(t) = max( G_{i-1}(t) [drop],
-//                       max_k G_{i-1}(min(t,d_i) - C_i(k)) + q_i(k) )
-//       with options invalid before the release masked by a NEG row value.
-//       Each thread owns columns t = m*NT + tid (m < COLS) and keeps its
-//       G_{i-1}(t) in registers (the drop option costs no shared-memory
-//       load); the option reads G_{i-1}(t - C_k) come from a shared-memory row
-//       (double-buffered, or single-buffered with a read/write barrier pair).
-//       One VIADDMNMX (__viaddmax_s32) per (cell, option) on packed keys
-//       carries the argmax in the low 4 bits, ties resolving to the smaller
-//       code (drop < 0 < 1 < ...).  4-bit decisions per cell go to shared
-//       memory or to a per-CTA global slab.
-//   a5  Q* = G_N(T), t* = least t with G_N(t) = Q*
-//   a6  backtrack through the decision nibbles
-//   a7  EDF schedule times, outputs in input order
-//   a8  batch statistics (one int64 atomic per slot per CTA)
+// Persistent grid; a CTA = NW "DP warps" + 1 "tail warp", one instance at a
+// time, warp-specialised so the DP warps only ever sweep the table:
+//
+//   tail warp  a1 descriptor loads + validation, a2 prefix sums C_i(k),
+//              R_i(k), Delta (P:L78 / Theorem 1), packed
+//              option keys, a3 EDF order (d, r, idx) by warp bitonic
+//              sort — all for instance b+1 while the DP warps sweep b;
+//              then a6 backtrack of b, a7 EDF schedule times
+//              via a warp max-plus scan and the outputs, a8 stats.
+//   DP warps   a4 the time-indexed dual of Eqs. 1-2:
+//                 G_i(t) = max( G_{i-1}(t) [drop],
+//                               max_k G_{i-1}(min(t,d_i) - C_i(k)) + q_i(k) )
+//              a5 Q* = G_N(T), t* by a 32-ary search.
+//
+// Two identities keep the sweep at one shared-memory load per (cell, option):
+//   * packed keys: a cell stores Q*16 + 15; option k adds (q_k << 4) - (k+1),
+//     so one VIADDMNMX (fused add+max) per option yields value *and* argmax
+//     (low nibble = 15 - code; ties resolve to the smaller code, drop first);
+//   * tail collapse: EDF rows are sorted by deadline, so for t > d_i every
+//     G_i(t) equals one constant M_i = max(M_{i-1}, A_i) with
+//     A_i = max_k G_{i-1}(d_i - C_i(k)) + q_i(k).  Only the active columns
+//     t <= d_i are swept; (d_i, d_{i+1}] is filled with M_i for the next row,
+//     and the tail decision is one nibble per row.
+// Threads own columns t = g*NT + tid, so every shifted read t - C_k is
+// conflict-free.  Rows are double-buffered, or (H = 32768) updated in place
+// chunk by chunk from high to low columns with a barrier per chunk.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <type_traits>
 
 namespace icsched {
 
 constexpr int NEG = -(1 << 30);
-constexpr int MAXK = 15;  // options per task: 0..14 optional stages
+constexpr int KMAX = 15;           // options per task: mandatory-only .. 14 optional stages
+constexpr int BAR_DP = 1, BAR_READY = 2, BAR_DONE = 3;
+constexpr int ST_OK = 0, ST_INFEASIBLE = 1, ST_BAD = 2, ST_LIMIT = 3, ST_END = -1;
 
 struct Params {
-  // inputs (device pointers)
   int64_t B;
   const int64_t* task_begin;
   const int32_t *release, *deadline, *mand_wcet;
@@ -42,7 +45,6 @@ struct Params {
   const int32_t* opt_wcet;
   const uint32_t* mand_conf;
   const int32_t* opt_gain;
-  // outputs
   int8_t* kept;
   int32_t *start, *finish;
   int64_t *q_total, *conf_micro;
@@ -50,92 +52,127 @@ struct Params {
   int32_t* makespan;
   uint8_t* status;
   unsigned long long* stats;
-  // config
-  int drop_mode;
   uint32_t delta_micro, eps_micro;
   int max_tasks, smax, H;
-  // geometry
-  int pad, nbuf, dec_smem, kp, np2max;
+  int pad, nq, kp, r1, np2;
+  int dec_smem;
   uint32_t* dec_global;
   int64_t dec_slab_words;
-  // shared-memory layout (byte offsets)
-  int off_rowbuf, off_dec, off_rowp, off_tR, off_info, off_key, off_tr, off_td, off_tS, off_chosen,
-      off_misc;
+  // shared-memory layout (byte offsets); slot arrays are [2][...]
+  int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
+      off_sS, off_key;
+  int nslots;  // 2: set up instance b+1 while the DP sweeps b; 1: serialised (large N)
+  int rowbuf_stride;  // ints per row buffer (pad + capacity)
 };
 
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
 
-// One DP row with exactly K valid options (compile-time), all COLS column groups.
-template <int NT, int COLS, int K, bool SB, typename RowPtr>
-__device__ __forceinline__ void dp_row(int (&G)[COLS], const Params& p, const int32_t* __restrict__ cur,
-                                       RowPtr nxt, uint32_t* __restrict__ decrow,
-                                       const int2* __restrict__ op, const int d, const int r_next,
-                                       const int store_lim, const bool has_next, const int ncols) {
-  constexpr bool single_buf = SB;
-  constexpr int NQ = (COLS + 7) / 8;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int C[K > 0 ? K : 1], key[K > 0 ? K : 1];
+// ---------------------------------------------------------------------------
+// DP warps: one row, active columns t <= d.  K options (compile-time; GEN =
+// general path with runtime kr options and per-option release masks).
+template <int NW, bool SB, bool DROP, int K, bool GEN>
+__device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
+                                       const int4* __restrict__ ops4, const int d, const int r, const int kr,
+                                       const int nq) {
+  constexpr int NT = 32 * NW;
+  constexpr int KK = GEN ? KMAX : K;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  int C[KK > 0 ? KK : 1], key[KK > 0 ? KK : 1];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int2 o = op[k];
-    C[k] = o.x;
-    key[k] = o.y;
-  }
-  // admit-only value at column d, used by every column t > d (min(t, d) = d)
-  int A = NEG;
-  if (K > 0 && d < ncols - 1) {
-    int v = NEG;
-    if (lane < K) {
-      const int2 o = op[lane];
-      v = cur[d - o.x] + o.y;
+  for (int k = 0; k < KK; k += 2) {
+    if (!GEN || k < kr) {
+      const int4 o = ops4[k >> 1];
+      C[k] = o.x;
+      key[k] = o.y;
+      if (k + 1 < KK) {
+        C[k + 1] = o.z;
+        key[k + 1] = o.w;
+      }
     }
-    A = __reduce_max_sync(0xffffffffu, v);
   }
   const int w0 = warp * 32;
-  const int mact = d >= w0 ? min(COLS, (d - w0) / NT + 1) : 0;  // groups holding a column t <= d
-  const int mlive = min(COLS, (ncols - 1 - w0) >= 0 ? (ncols - 1 - w0) / NT + 1 : 0);
-  uint32_t dw[NQ];
+  const int ng = d >= w0 ? (d - w0) / NT + 1 : 0;  // this warp's groups holding a column t <= d
+  auto cell = [&](int t) -> int {
+    int v = DROP ? cur[t] : NEG;
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) dw[q] = 0;
-#pragma unroll
-  for (int m = 0; m < COLS; ++m) {
-    if (m < mlive) {
-      const int t = m * NT + tid;
-      const int drop = p.drop_mode ? NEG : (G[m] | 15);
-      int v = drop;
-      if (m < mact) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) v = viaddmax(cur[t - C[k]], key[k], v);
-      }
-      const int tail = max(drop, A);
-      v = (t <= d) ? v : tail;
-      dw[m >> 3] |= (uint32_t)(v & 15) << (4 * (m & 7));
-      G[m] = v & ~15;
-      if (!single_buf && has_next && m * NT + w0 <= store_lim) nxt[t] = (t >= r_next) ? G[m] : NEG;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) decrow[q * NT + tid] = dw[q];
-  if (single_buf) {
-    __syncthreads();  // every read of the row is done before it is overwritten
-    if (has_next) {
-#pragma unroll
-      for (int m = 0; m < COLS; ++m) {
-        const int t = m * NT + tid;
-        if (m < mlive && m * NT + w0 <= store_lim) nxt[t] = (t >= r_next) ? G[m] : NEG;
+    for (int k = 0; k < KK; ++k) {
+      if (GEN) {
+        if (k < kr) {
+          const int src = t - C[k];
+          if (src >= r) v = viaddmax(cur[src], key[k], v);
+        }
+      } else {
+        v = viaddmax(cur[t - C[k]], key[k], v);
       }
     }
+    return v;
+  };
+  if (!SB) {
+    for (int g0 = 0; g0 < ng; g0 += 8) {
+      const int tb = g0 * NT + tid;
+      uint32_t dw = 0;
+      if (g0 + 8 <= ng) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = cell(tb + u * NT);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          dw |= (uint32_t)(v[u] & 15) << (4 * u);
+          nxt[tb + u * NT] = v[u] | 15;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (g0 + u < ng) {
+            const int v = cell(tb + u * NT);
+            dw |= (uint32_t)(v & 15) << (4 * u);
+            nxt[tb + u * NT] = v | 15;
+          }
+        }
+      }
+      decrow[(g0 >> 3) * NT + tid] = dw;
+    }
+  } else {
+    // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
+    // chunk c reads only columns below its top, so writing it after the barrier
+    // cannot disturb a lower chunk still to be computed.
+    const int nch = d >= 0 ? (d / NT) / 8 + 1 : 0;  // CTA-uniform chunk count (warp 0 has the most groups)
+    for (int c = nch - 1; c >= 0; --c) {
+      const int g0 = c * 8;
+      const int tb = g0 * NT + tid;
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT) : 0;
+      bar_sync(BAR_DP, NT);
+      uint32_t dw = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (g0 + u < ng) {
+          dw |= (uint32_t)(v[u] & 15) << (4 * u);
+          nxt[tb + u * NT] = v[u] | 15;
+        }
+      }
+      if (g0 < ng) decrow[(g0 >> 3) * NT + tid] = dw;
+    }
   }
+  (void)nq;
 }
 
-template <int NT, int COLS, bool SB>
-__device__ __forceinline__ void dp_row_dispatch(int K, int (&G)[COLS], const Params& p, const int32_t* cur,
-                                                int32_t* nxt, uint32_t* decrow, const int2* op, int d,
-                                                int r_next, int store_lim, bool has_next, int ncols) {
-  // double-buffered rows never alias: let the compiler interleave loads and stores freely
-  using RowPtr = typename std::conditional<SB, int32_t*, int32_t* __restrict__>::type;
+template <int NW, bool SB, bool DROP>
+__device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
+                                                uint32_t* decrow, const int4* ops4, int d, int r, int nq) {
+  if (gen) {
+    dp_row<NW, SB, DROP, KMAX, true>(cur, nxt, decrow, ops4, d, r, K, nq);
+    return;
+  }
 #define IC_ROW(KK) \
-  case KK: dp_row<NT, COLS, KK, SB, RowPtr>(G, p, cur, nxt, decrow, op, d, r_next, store_lim, has_next, ncols); break;
+  case KK: dp_row<NW, SB, DROP, KK, false>(cur, nxt, decrow, ops4, d, r, K, nq); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -144,62 +181,8 @@ __device__ __forceinline__ void dp_row_dispatch(int K, int (&G)[COLS], const Par
 #undef IC_ROW
 }
 
-// Slow path for rows whose longest usable option reaches further left than
-// the NEG pad: source index clamped per lane to -1 (a NEG cell).
-template <int NT, int COLS, bool SB>
-__device__ __forceinline__ void dp_row_general(int K, int (&G)[COLS], const Params& p, const int32_t* cur,
-                                               int32_t* nxt, uint32_t* decrow, const int2* op, int d,
-                                               int r_next, int store_lim, bool has_next, int ncols) {
-  constexpr bool single_buf = SB;
-  constexpr int NQ = (COLS + 7) / 8;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int A = NEG;
-  if (K > 0 && d < ncols - 1) {
-    int v = NEG;
-    if (lane < K) {
-      const int2 o = op[lane];
-      v = cur[d - o.x] + o.y;
-    }
-    A = __reduce_max_sync(0xffffffffu, v);
-  }
-  const int w0 = warp * 32;
-  uint32_t dw[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) dw[q] = 0;
-#pragma unroll
-  for (int m = 0; m < COLS; ++m) {
-    const int t = m * NT + tid;
-    if (m * NT + w0 <= ncols - 1) {
-      const int drop = p.drop_mode ? NEG : (G[m] | 15);
-      int v = drop;
-      if (t <= d) {
-        for (int k = 0; k < K; ++k) {
-          const int2 o = op[k];
-          v = viaddmax(cur[max(t - o.x, -1)], o.y, v);
-        }
-      } else {
-        v = max(drop, A);
-      }
-      dw[m >> 3] |= (uint32_t)(v & 15) << (4 * (m & 7));
-      G[m] = v & ~15;
-      if (!single_buf && has_next && m * NT + w0 <= store_lim) nxt[t] = (t >= r_next) ? G[m] : NEG;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) decrow[q * NT + tid] = dw[q];
-  if (single_buf) {
-    __syncthreads();
-    if (has_next) {
-#pragma unroll
-      for (int m = 0; m < COLS; ++m) {
-        const int t = m * NT + tid;
-        if (m * NT + w0 <= ncols - 1 && m * NT + w0 <= store_lim) nxt[t] = (t >= r_next) ? G[m] : NEG;
-      }
-    }
-  }
-}
-
-// Warp-level bitonic sort of up to 32 64-bit keys (one per lane), ascending.
+// ---------------------------------------------------------------------------
+// Tail warp helpers.
 __device__ __forceinline__ unsigned long long warp_bitonic_sort(unsigned long long x, int lane) {
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
@@ -208,298 +191,471 @@ __device__ __forceinline__ unsigned long long warp_bitonic_sort(unsigned long lo
       const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, j);
       const bool up = ((lane & k) == 0);
       const bool lower = ((lane & j) == 0);
-      const bool take_min = (lower == up);
-      x = take_min ? (x < y ? x : y) : (x < y ? y : x);
+      x = (lower == up) ? (x < y ? x : y) : (x < y ? y : x);
     }
   }
   return x;
 }
 
-template <int NT, int COLS, bool SB>
-__global__ void __launch_bounds__(NT) ic_dp_kernel(const Params p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int NQ = (COLS + 7) / 8;
-  constexpr int CAP = NT * COLS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int32_t* rowbuf = (int32_t*)(smem + p.off_rowbuf);
-  uint32_t* dec = p.dec_smem ? (uint32_t*)(smem + p.off_dec)
-                             : p.dec_global + (int64_t)blockIdx.x * p.dec_slab_words;
-  int2* rowp = (int2*)(smem + p.off_rowp);
-  int32_t* tR = (int32_t*)(smem + p.off_tR);
-  int4* info = (int4*)(smem + p.off_info);
-  unsigned long long* skey = (unsigned long long*)(smem + p.off_key);
-  int32_t* tr = (int32_t*)(smem + p.off_tr);
-  int32_t* td = (int32_t*)(smem + p.off_td);
-  int32_t* tS = (int32_t*)(smem + p.off_tS);
-  int32_t* chosen = (int32_t*)(smem + p.off_chosen);
-  int32_t* misc = (int32_t*)(smem + p.off_misc);
-  unsigned long long* misc64 = (unsigned long long*)(smem + p.off_misc + 64);
-  const int RS = p.pad + CAP;
-  const int R1 = p.smax + 1;
-  constexpr bool single_buf = SB;
-
-  for (int bb = 0; bb < p.nbuf; ++bb)
-    for (int i = tid; i < p.pad; i += NT) rowbuf[bb * RS + i] = NEG;
-
-  unsigned long long acc[8];
+__device__ __forceinline__ long long warp_sum64(long long v) {
 #pragma unroll
-  for (int s = 0; s < 8; ++s) acc[s] = 0;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
-  for (int64_t b = blockIdx.x; b < p.B; b += gridDim.x) {
-    const int64_t lo = p.task_begin[b];
-    const int64_t n64 = p.task_begin[b + 1] - lo;
-    if (tid == 0) {
-      misc[0] = 0;          // Rmax
-      misc[1] = 0;          // dmax (T = max(0, max d))
-      misc[2] = 0x7fffffff; // t*
-      misc[3] = 0;          // Q* packed
-      misc64[0] = 0;        // sum_i max_k q
-    }
-    __syncthreads();
-    const bool too_many = n64 < 0 || n64 > p.max_tasks;
-    const int n = too_many ? 0 : (int)n64;
+struct Smem {
+  int32_t* rowbuf;
+  uint32_t* dec;
+  int2* rowp;    // [2][max_tasks][kp]  (C_k, key_k) of EDF row pos
+  int4* info;    // [2][max_tasks]      (d, K | gen<<8 | S<<16, r, d_next)
+  int32_t* tR;   // [2][max_tasks][r1]  cumulative confidence of EDF row pos
+  int32_t* task; // [2][max_tasks]      input index of EDF row pos
+  int32_t* tail; // [2][max_tasks]      tail nibble of row pos
+  long long* misc;  // [2][16]
+  int32_t* chosen;  // [max_tasks]
+  int32_t *sd, *sr, *sS;  // staging (input order), tail warp only
+  unsigned long long* key;
+};
 
-    // ---- a1/a2: descriptors, validation, prefix sums, feasible-reward max
-    int bad = too_many ? 1 : 0;
-    int rmax_l = 0, dmax_l = 0;
-    for (int i = tid; i < n; i += NT) {
-      const int64_t t = lo + i;
-      const int r = p.release[t], d = p.deadline[t], m = p.mand_wcet[t];
-      const int S = p.n_opt[t];
-      const uint32_t a0 = p.mand_conf[t];
-      int tb = (S > p.smax) | (r < 0) | (d >= p.H) | (m < 1) | (a0 > 1000000u);
-      tr[i] = r;
-      td[i] = d;
-      tS[i] = S;
-      dmax_l = max(dmax_l, d);
-      if (!tb) {
-        int64_t C = m, R = a0;
-        for (int k = 0; k <= S; ++k) {
-          if (k > 0) {
-            const int w = p.opt_wcet[t * p.smax + (k - 1)];
-            const int g = p.opt_gain[t * p.smax + (k - 1)];
-            tb |= (w < 1);
-            C += w;
-            R += g;
-            tb |= (R < 0) | (R > 1000000);
-          }
-          rowp[i * p.kp + k].x = (int)min(C, (int64_t)(1 << 30));
-          tR[i * R1 + k] = (int)R;
-          if ((int64_t)r + C <= d && R > rmax_l) rmax_l = (int)R;
-        }
-      }
-      bad |= tb;
-    }
-    bad = __syncthreads_or(bad);
-    if (!bad) {
-      atomicMax(&misc[0], rmax_l);
-      atomicMax(&misc[1], dmax_l);
-    }
-    __syncthreads();
-    int64_t delta = 1;
-    if (p.delta_micro > 0) {
-      delta = p.delta_micro;
-    } else if (n > 0) {
-      delta = ((int64_t)p.eps_micro * (int64_t)misc[0]) / (1000000LL * n);
-      if (delta < 1) delta = 1;
-    }
-    if (!bad) {
-      for (int i = tid; i < n; i += NT) {
-        const int S = tS[i], d = td[i];
-        int qmax = 0;
-        for (int k = 0; k <= S; ++k) {
-          const int q = (int)(tR[i * R1 + k] / delta);
-          qmax = max(qmax, q);
-          rowp[i * p.kp + k].y = (q << 4) | (14 - k);
-        }
-        atomicAdd(&misc64[0], (unsigned long long)qmax);
-        const uint32_t dk = (uint32_t)d ^ 0x80000000u;
-        const uint32_t rk = (uint32_t)min(tr[i], (1 << 20) - 1);
-        skey[i] = ((unsigned long long)dk << 32) | ((unsigned long long)rk << 12) | (unsigned)i;
-      }
-    }
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    for (int i = n + tid; i < np2; i += NT) skey[i] = ~0ull;
-    __syncthreads();
-    const bool limit = !bad && (misc64[0] * 16ull + 16ull * (unsigned long long)n >= (1ull << 30));
-
-    if (bad || limit) {
-      // ---- per-instance error: everything dropped, status says why
-      for (int64_t i = tid; i < n64; i += NT) {
-        p.kept[lo + i] = -1;
-        p.start[lo + i] = -1;
-        p.finish[lo + i] = -1;
-      }
-      if (tid == 0) {
-        p.q_total[b] = 0;
-        p.conf_micro[b] = 0;
-        p.conf_total[b] = 0.0;
-        p.makespan[b] = 0;
-        p.status[b] = bad ? 2 : 3;
-        acc[0] += 1;
-        acc[3] += 1;
-      }
-      __syncthreads();
-      continue;
-    }
-
-    // ---- a3: EDF order (d, r, idx)
-    if (np2 <= 32) {
-      if (warp == 0) {
-        unsigned long long x = lane < np2 ? skey[lane] : ~0ull;
-        x = warp_bitonic_sort(x, lane);
-        if (lane < np2) skey[lane] = x;
-      }
-    } else {
-      for (int k = 2; k <= np2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = tid; i < np2; i += NT) {
-            const int ixj = i ^ j;
-            if (ixj > i) {
-              const unsigned long long a = skey[i], c = skey[ixj];
-              const bool up = (i & k) == 0;
-              if ((a > c) == up) {
-                skey[i] = c;
-                skey[ixj] = a;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      }
-    }
-    __syncthreads();
-    for (int pos = tid; pos < n; pos += NT) {
-      const int task = (int)(skey[pos] & 0xFFF);
-      const int d = td[task], S = tS[task];
-      int K = 0;
-      while (K <= S && rowp[task * p.kp + K].x <= d) ++K;  // options with C_k <= d
-      int r_next = 0, store_lim = -0x7fffffff;
-      if (pos + 1 < n) {
-        const int t2 = (int)(skey[pos + 1] & 0xFFF);
-        r_next = tr[t2];
-        store_lim = td[t2] - rowp[t2 * p.kp].x;  // the next row reads sources <= d' - C'(0)
-      }
-      const int fast = (K == 0 || rowp[task * p.kp + K - 1].x <= p.pad) ? 1 : 0;
-      info[pos] = make_int4(d, r_next, (task << 8) | (fast << 7) | K, store_lim);
-    }
-    const int ncols = misc[1] + 1;
-    {
-      const int r0 = n > 0 ? tr[(int)(skey[0] & 0xFFF)] : 0;
-      int32_t* buf0 = rowbuf + p.pad;
-      for (int t = tid; t < ncols; t += NT) buf0[t] = (t >= r0) ? 0 : NEG;
-    }
-    __syncthreads();
-
-    // ---- a4: the DP sweep
-    int G[COLS];
-#pragma unroll
-    for (int m = 0; m < COLS; ++m) G[m] = 0;
-    for (int pos = 0; pos < n; ++pos) {
-      const int4 inf = info[pos];
-      const int d = inf.x, r_next = inf.y, task = inf.z >> 8, K = inf.z & 0x7F;
-      const bool fast = (inf.z >> 7) & 1;
-      const int32_t* cur = rowbuf + (single_buf ? 0 : (pos & 1)) * RS + p.pad;
-      int32_t* nxt = rowbuf + (single_buf ? 0 : ((pos + 1) & 1)) * RS + p.pad;
-      uint32_t* decrow = dec + (int64_t)pos * NQ * NT;
-      const int2* op = rowp + task * p.kp;
-      const bool has_next = pos + 1 < n;
-      if (fast)
-        dp_row_dispatch<NT, COLS, SB>(K, G, p, cur, nxt, decrow, op, d, r_next, inf.w, has_next, ncols);
-      else
-        dp_row_general<NT, COLS, SB>(K, G, p, cur, nxt, decrow, op, d, r_next, inf.w, has_next, ncols);
-      __syncthreads();
-    }
-
-    // ---- a5: Q* = G_N(T), t* = least t attaining it
-    {
-      const int tl = ncols - 1;
-#pragma unroll
-      for (int m = 0; m < COLS; ++m)
-        if (m * NT + tid == tl) misc[3] = n > 0 ? G[m] : 0;
-    }
-    __syncthreads();
-    const int Qp = misc[3];
-    {
-      int best = 0x7fffffff;
-#pragma unroll
-      for (int m = COLS - 1; m >= 0; --m) {
-        const int t = m * NT + tid;
-        if (t < ncols && G[m] == Qp) best = t;
-      }
-      if (n == 0) best = 0;
-      if (best != 0x7fffffff) atomicMin(&misc[2], best);
-    }
-    __syncthreads();
-
-    // ---- a6/a7: backtrack and the EDF schedule, by one thread
-    if (tid == 0) {
-      const bool feasible = Qp >= 0;
-      int t = misc[2];
-      if (feasible) {
-        for (int pos = n - 1; pos >= 0; --pos) {
-          const int m = t / NT, tt = t - m * NT;
-          const uint32_t w = dec[((int64_t)pos * NQ + (m >> 3)) * NT + tt];
-          const int code = 15 - (int)((w >> (4 * (m & 7))) & 15u);
-          chosen[pos] = code;
-          if (code > 0) {
-            const int4 inf = info[pos];
-            const int task = inf.z >> 8;
-            t = min(t, inf.x) - rowp[task * p.kp + code - 1].x;
-          }
-        }
-      }
-      int64_t F = 0, Q = 0, conf = 0;
-      int ndrop = 0, nopt = 0, noff = 0;
-      for (int pos = 0; pos < n; ++pos) {
-        const int4 inf = info[pos];
-        const int task = inf.z >> 8;
-        noff += tS[task];
-        const int code = feasible ? chosen[pos] : 0;
-        if (code > 0) {
-          const int k = code - 1;
-          const int2 o = rowp[task * p.kp + k];
-          const int64_t s = max(F, (int64_t)tr[task]);
-          const int64_t f = s + o.x;
-          p.kept[lo + task] = (int8_t)k;
-          p.start[lo + task] = (int32_t)s;
-          p.finish[lo + task] = (int32_t)f;
-          F = f;
-          Q += o.y >> 4;
-          conf += tR[task * R1 + k];
-          nopt += k;
-        } else {
-          p.kept[lo + task] = -1;
-          p.start[lo + task] = -1;
-          p.finish[lo + task] = -1;
-          ++ndrop;
-        }
-      }
-      p.q_total[b] = Q;
-      p.conf_micro[b] = conf;
-      p.conf_total[b] = (double)conf / 1e6;
-      p.makespan[b] = (int32_t)F;
-      p.status[b] = feasible ? 0 : 1;
-      acc[0] += 1;
-      if (feasible) {
-        acc[1] += n;
-        acc[2] += ndrop;
-        acc[4] += nopt;
-        acc[5] += noff;
-        acc[6] += conf;
-        acc[7] += Q;
-      } else {
-        acc[3] += 1;
-      }
-    }
-    __syncthreads();
+// Write the "everything dropped" outputs of an instance that the DP never sees.
+__device__ __forceinline__ void write_dropped(const Params& p, int64_t b, int64_t lo, int64_t n, int status,
+                                              int lane) {
+  for (int64_t i = lane; i < n; i += 32) {
+    p.kept[lo + i] = -1;
+    p.start[lo + i] = -1;
+    p.finish[lo + i] = -1;
   }
-  if (tid == 0 && p.stats) {
-#pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (acc[s]) atomicAdd(&p.stats[s], acc[s]);
+  if (lane == 0) {
+    p.q_total[b] = 0;
+    p.conf_micro[b] = 0;
+    p.conf_total[b] = 0.0;
+    p.makespan[b] = 0;
+    p.status[b] = (uint8_t)status;
   }
 }
+
+// Load task t's optional WCETs and gains (up to KMAX-1, predicated on S).
+__device__ __forceinline__ void load_opt(const Params& p, int64_t t, int Sn, int (&w)[KMAX - 1],
+                                         int (&g)[KMAX - 1]) {
+#pragma unroll
+  for (int k = 0; k < KMAX - 1; ++k) {
+    if (k < Sn) {
+      w[k] = p.opt_wcet[t * p.smax + k];
+      g[k] = p.opt_gain[t * p.smax + k];
+    }
+  }
+}
+
+// a1-a3 for instance b into slot s.  Returns ST_OK if the DP must run it;
+// otherwise the outputs are already written (bad input, limit, empty set).
+// Pass 1 (input order): validation, the best individually feasible reward
+// (Theorem 1's R), the EDF keys.  Pass 2 (EDF order, descriptors re-read):
+// prefix sums, q = R div Delta, packed keys, the row table of the DP.
+template <int NW>
+__device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int lane,
+                          unsigned long long (&acc)[8]) {
+  const int64_t lo = p.task_begin[b];
+  const int64_t n64 = p.task_begin[b + 1] - lo;
+  if (n64 < 0 || n64 > p.max_tasks) {
+    write_dropped(p, b, lo, n64 > 0 ? n64 : 0, ST_BAD, lane);
+    if (lane == 0) { acc[0] += 1; acc[3] += 1; }
+    return ST_BAD;
+  }
+  const int n = (int)n64;
+  if (n == 0) {
+    write_dropped(p, b, lo, 0, ST_OK, lane);
+    if (lane == 0) acc[0] += 1;
+    return ST_BAD + 100;  // handled (empty task set: Q = 0, status OK)
+  }
+  int bad = 0, rmax = 0;
+  for (int i = lane; i < n; i += 32) {
+    const int64_t t = lo + i;
+    const int r = p.release[t], d = p.deadline[t], m = p.mand_wcet[t];
+    const int Sn = p.n_opt[t];
+    const uint32_t a0 = p.mand_conf[t];
+    int tb = (Sn > p.smax) | (r < 0) | (d >= p.H) | (m < 1) | (a0 > 1000000u);
+    S.sd[i] = d;
+    S.sr[i] = r;
+    S.sS[i] = Sn;
+    if (!tb) {
+      int w[KMAX - 1], g[KMAX - 1];
+      load_opt(p, t, Sn, w, g);
+      long long C = m, R = a0;
+      if ((long long)r + C <= d && R > rmax) rmax = (int)R;
+#pragma unroll
+      for (int k = 0; k < KMAX - 1; ++k) {
+        if (k < Sn) {
+          tb |= (w[k] < 1);
+          C += w[k];
+          R += g[k];
+          tb |= (R < 0) | (R > 1000000);
+          if ((long long)r + C <= d && R > rmax) rmax = (int)R;
+        }
+      }
+    }
+    bad |= tb;
+    const uint32_t dk = (uint32_t)d ^ 0x80000000u;
+    const uint32_t rk = (uint32_t)min(max(r, 0), (1 << 20) - 1);
+    S.key[i] = ((unsigned long long)dk << 32) | ((unsigned long long)rk << 12) | (unsigned)i;
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad) {
+    write_dropped(p, b, lo, n, ST_BAD, lane);
+    if (lane == 0) { acc[0] += 1; acc[3] += 1; }
+    return ST_BAD;
+  }
+  rmax = __reduce_max_sync(0xffffffffu, rmax);
+  long long delta = p.delta_micro;
+  if (delta == 0) {
+    delta = ((long long)p.eps_micro * rmax) / (1000000LL * n);
+    if (delta < 1) delta = 1;
+  }
+  // a3: EDF order
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  if (np2 <= 32) {
+    unsigned long long x = lane < n ? S.key[lane] : ~0ull;
+    x = warp_bitonic_sort(x, lane);
+    if (lane < n) S.key[lane] = x;
+  } else {
+    for (int i = n + lane; i < np2; i += 32) S.key[i] = ~0ull;
+    __syncwarp();
+    for (int k = 2; k <= np2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < np2; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long a = S.key[i], c = S.key[ixj];
+            if ((a > c) == ((i & k) == 0)) {
+              S.key[i] = c;
+              S.key[ixj] = a;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  // pass 2: the row table in EDF order
+  long long qsum = 0;
+  for (int pos = lane; pos < n; pos += 32) {
+    const int tk = (int)(S.key[pos] & 0xFFF);
+    const int64_t t = lo + tk;
+    const int d = S.sd[tk], r = S.sr[tk], Sn = S.sS[tk];
+    int w[KMAX - 1], g[KMAX - 1];
+    load_opt(p, t, Sn, w, g);
+    int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
+    int32_t* trp = S.tR + ((size_t)s * p.max_tasks + pos) * p.r1;
+    long long C = p.mand_wcet[t], R = p.mand_conf[t];
+    int K = 0, qmax = 0, clast = 0;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k <= Sn) {
+        if (k > 0) {
+          C += w[k - 1];
+          R += g[k - 1];
+        }
+        const int q = (int)(R / delta);
+        qmax = max(qmax, q);
+        if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
+          rp[k] = make_int2((int)C, (q << 4) - (k + 1));
+          trp[k] = (int)R;
+          K = k + 1;
+          clast = (int)C;
+        }
+      }
+    }
+    qsum += qmax;
+    const bool gen = (r > 0) || (K > 0 && clast > p.pad);
+    const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
+    S.info[s * p.max_tasks + pos] = make_int4(d, K | (gen ? 256 : 0) | (Sn << 16), r, dn);
+    S.task[s * p.max_tasks + pos] = tk;
+  }
+  qsum = warp_sum64(qsum);
+  if (qsum * 16 + 16LL * n >= (1LL << 30)) {
+    write_dropped(p, b, lo, n, ST_LIMIT, lane);
+    if (lane == 0) { acc[0] += 1; acc[3] += 1; }
+    return ST_LIMIT;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    long long* mi = S.misc + s * 16;
+    mi[0] = n;
+    mi[1] = lo;
+    mi[2] = b;
+    mi[3] = ST_OK;
+    mi[4] = delta;
+    mi[7] = S.info[s * p.max_tasks].x;
+    mi[8] = S.info[s * p.max_tasks + n - 1].x;
+  }
+  __syncwarp();
+  return ST_OK;
+}
+
+// a6: backtrack from (Q*, t*) through the decision nibbles (one lane).
+template <int NW>
+__device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, int s, int lane) {
+  constexpr int NT = 32 * NW;
+  const long long* mi = S.misc + s * 16;
+  const int n = (int)mi[0];
+  if (lane == 0) {
+    if (mi[5] >= 0) {
+      int t = (int)mi[6];
+      const int4* inf = S.info + s * p.max_tasks;
+      const int2* rp = S.rowp + (size_t)s * p.max_tasks * p.kp;
+      for (int pos = n - 1; pos >= 0; --pos) {
+        const int d = inf[pos].x;
+        int nib;
+        if (t > d) {
+          nib = S.tail[s * p.max_tasks + pos];
+        } else {
+          const int g = t / NT, l = t - g * NT;
+          const uint32_t w = S.dec[((size_t)pos * p.nq + (g >> 3)) * NT + l];
+          nib = (int)((w >> (4 * (g & 7))) & 15u);
+        }
+        const int code = 15 - nib;
+        S.chosen[pos] = code;
+        if (code > 0) t = min(t, d) - rp[(size_t)pos * p.kp + code - 1].x;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// a7/a8: EDF schedule (warp max-plus scan), outputs in input order, stats.
+__device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int s, int lane,
+                                             unsigned long long (&acc)[8]) {
+  const long long* mi = S.misc + s * 16;
+  const int n = (int)mi[0];
+  const int64_t lo = mi[1], b = mi[2];
+  const bool feasible = mi[5] >= 0;
+  const int4* inf = S.info + s * p.max_tasks;
+  long long F = 0, Q = 0, conf = 0, ndrop = 0, nopt = 0, noff = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int pos = base + lane;
+    const bool valid = pos < n;
+    int code = 0, tk = 0, Cc = 0, r = 0, Sn = 0;
+    if (valid) {
+      const int4 f = inf[pos];
+      r = f.z;
+      Sn = f.y >> 16;
+      tk = S.task[s * p.max_tasks + pos];
+      code = feasible ? S.chosen[pos] : 0;
+    }
+    long long a = 0, bb = -(1LL << 62);  // map x -> max(x + a, bb)
+    if (code > 0) {
+      const int2 o = S.rowp[((size_t)s * p.max_tasks + pos) * p.kp + code - 1];
+      Cc = o.x;
+      a = Cc;
+      bb = (long long)r + Cc;
+      Q += (o.y + code) >> 4;
+      conf += S.tR[((size_t)s * p.max_tasks + pos) * p.r1 + code - 1];
+      nopt += code - 1;
+    } else if (valid) {
+      ndrop += 1;
+    }
+    noff += Sn;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // inclusive scan of map composition
+      const long long a2 = __shfl_up_sync(0xffffffffu, a, o);
+      const long long b2 = __shfl_up_sync(0xffffffffu, bb, o);
+      if (lane >= o) {
+        bb = max(b2 + a, bb);
+        a = a2 + a;
+      }
+    }
+    const long long f = max(F + a, bb);
+    if (valid) {
+      if (code > 0) {
+        p.kept[lo + tk] = (int8_t)(code - 1);
+        p.start[lo + tk] = (int32_t)(f - Cc);
+        p.finish[lo + tk] = (int32_t)f;
+      } else {
+        p.kept[lo + tk] = -1;
+        p.start[lo + tk] = -1;
+        p.finish[lo + tk] = -1;
+      }
+    }
+    F = __shfl_sync(0xffffffffu, f, 31);
+  }
+  Q = warp_sum64(Q);
+  conf = warp_sum64(conf);
+  ndrop = warp_sum64(ndrop);
+  nopt = warp_sum64(nopt);
+  noff = warp_sum64(noff);
+  if (lane == 0) {
+    p.q_total[b] = Q;
+    p.conf_micro[b] = conf;
+    p.conf_total[b] = (double)conf / 1e6;
+    p.makespan[b] = (int32_t)F;
+    p.status[b] = feasible ? ST_OK : ST_INFEASIBLE;
+    acc[0] += 1;
+    if (feasible) {
+      acc[1] += n;
+      acc[2] += ndrop;
+      acc[4] += nopt;
+      acc[5] += noff;
+      acc[6] += conf;
+      acc[7] += Q;
+    } else {
+      acc[3] += 1;
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+template <int NW, bool SB, bool DROP>
+__global__ void __launch_bounds__(32 * (NW + 1)) ic_dp_kernel(const Params p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int NT = 32 * NW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Smem S;
+  S.rowbuf = (int32_t*)(smem + p.off_rowbuf);
+  S.dec = p.dec_smem ? (uint32_t*)(smem + p.off_dec) : p.dec_global + (int64_t)blockIdx.x * p.dec_slab_words;
+  S.rowp = (int2*)(smem + p.off_rowp);
+  S.info = (int4*)(smem + p.off_info);
+  S.tR = (int32_t*)(smem + p.off_tR);
+  S.task = (int32_t*)(smem + p.off_task);
+  S.tail = (int32_t*)(smem + p.off_tail);
+  S.misc = (long long*)(smem + p.off_misc);
+  S.chosen = (int32_t*)(smem + p.off_chosen);
+  S.sd = (int32_t*)(smem + p.off_sd);
+  S.sr = (int32_t*)(smem + p.off_sr);
+  S.sS = (int32_t*)(smem + p.off_sS);
+  S.key = (unsigned long long*)(smem + p.off_key);
+  const int RS = p.rowbuf_stride;
+  for (int bb = 0; bb < (SB ? 1 : 2); ++bb)
+    for (int i = tid; i < p.pad; i += blockDim.x) S.rowbuf[bb * RS + i] = NEG;
+  __syncthreads();
+
+  if (warp == NW) {
+    // ================= tail warp =================
+    unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t b = blockIdx.x;
+    while (b < p.B && tail_setup<NW>(p, S, b, 0, lane, acc) != ST_OK) b += gridDim.x;
+    if (b >= p.B && lane == 0) S.misc[3] = ST_END;
+    __syncwarp();
+    bar_arrive(BAR_READY, NT + 32);
+    if (p.nslots == 2) {
+      int it = 0;
+      while (b < p.B) {
+        const int s = it & 1;
+        int64_t nb = b + gridDim.x;
+        while (nb < p.B && tail_setup<NW>(p, S, nb, s ^ 1, lane, acc) != ST_OK) nb += gridDim.x;
+        if (nb >= p.B && lane == 0) S.misc[(s ^ 1) * 16 + 3] = ST_END;
+        __syncwarp();
+        bar_sync(BAR_DONE, NT + 32);  // the DP warps finished instance b
+        tail_backtrack<NW>(p, S, s, lane);
+        bar_arrive(BAR_READY, NT + 32);  // decisions free: the DP warps may start nb
+        tail_outputs(p, S, s, lane, acc);
+        b = nb;
+        ++it;
+      }
+    } else {
+      while (b < p.B) {
+        bar_sync(BAR_DONE, NT + 32);
+        tail_backtrack<NW>(p, S, 0, lane);
+        tail_outputs(p, S, 0, lane, acc);
+        int64_t nb = b + gridDim.x;
+        while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb += gridDim.x;
+        if (nb >= p.B && lane == 0) S.misc[3] = ST_END;
+        __syncwarp();
+        bar_arrive(BAR_READY, NT + 32);
+        b = nb;
+      }
+    }
+    if (lane == 0 && p.stats) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (acc[i]) atomicAdd(&p.stats[i], acc[i]);
+    }
+    return;
+  }
+
+  // ================= DP warps =================
+  const int RSb = SB ? 0 : RS;
+  int32_t* buf0 = S.rowbuf + p.pad;
+  for (int it = 0;; ++it) {
+    bar_sync(BAR_READY, NT + 32);
+    const int s = p.nslots == 2 ? (it & 1) : 0;
+    long long* mi = S.misc + s * 16;
+    if (mi[3] == ST_END) break;
+    const int n = (int)mi[0];
+    const int d_first = (int)mi[7];
+    for (int t = tid; t <= d_first; t += NT) buf0[t] = 15;  // G_0(t) = 0
+    bar_sync(BAR_DP, NT);
+    const int4* inf = S.info + s * p.max_tasks;
+    const int2* rpb = S.rowp + (size_t)s * p.max_tasks * p.kp;
+    int M = 15;
+    for (int pos = 0; pos < n; ++pos) {
+      const int4 f = inf[pos];
+      const int d = f.x, K = f.y & 255, r = f.z, dn = f.w;
+      const bool gen = (f.y >> 8) & 1;
+      const int32_t* cur = buf0 + (pos & 1) * RSb;
+      int32_t* nxt = buf0 + ((pos + 1) & 1) * RSb;
+      const int2* ops = rpb + (size_t)pos * p.kp;
+      // admit value at column d: every column t > d shares it (tail collapse)
+      int av = NEG;
+      if (lane < K) {
+        const int2 o = ops[lane];
+        const int src = d - o.x;
+        if (src >= r) av = cur[src] + o.y;
+      }
+      const int A = __reduce_max_sync(0xffffffffu, av);
+      const int Mv = DROP ? max(M, A) : A;
+      if (tid == 0) S.tail[s * p.max_tasks + pos] = Mv & 15;
+      const int Mn = Mv | 15;
+      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, S.dec + (size_t)pos * p.nq * NT,
+                                    (const int4*)ops, d, r, p.nq);
+      // G_pos(t) = M_pos on (d, d_next]: the next row reads it there
+      if (pos + 1 < n) {
+        const int first = d + 1 > 0 ? d + 1 : 0;
+        int t = first + ((tid - first) % NT + NT) % NT;
+        for (; t <= dn; t += NT) nxt[t] = Mn;
+      }
+      M = Mn;
+      bar_sync(BAR_DP, NT);
+    }
+    // a5: Q* = G_N(T), t* = least t with G_N(t) = Q*  (G_N non-decreasing on [0, d_N])
+    if (warp == 0) {
+      const int dl = (int)mi[8];
+      const int32_t* fin = buf0 + (n & 1) * RSb;
+      long long Qv, ts = 0;
+      if (dl < 0) {
+        Qv = M;
+      } else {
+        Qv = fin[dl];
+        int lo = 0, hi = dl;  // predicate fin[t] >= Qv is false below t*, true from t*
+        while (lo < hi) {
+          const int step = (hi - lo + 32) / 32;
+          int x = lo + (lane + 1) * step - 1;
+          if (x > hi) x = hi;
+          const unsigned m = __ballot_sync(0xffffffffu, fin[x] >= Qv);
+          const int fl = __ffs(m) - 1;
+          const int nhi = fl == 0 ? min(lo + step - 1, hi) : min(lo + (fl + 1) * step - 1, hi);
+          const int nlo = fl == 0 ? lo : lo + fl * step;
+          lo = nlo;
+          hi = nhi;
+        }
+        ts = lo;
+      }
+      if (lane == 0) {
+        mi[5] = Qv >= 0 ? (Qv >> 4) : -1;
+        mi[6] = ts;
+      }
+    }
+    bar_sync(BAR_DP, NT);
+    bar_arrive(BAR_DONE, NT + 32);
+  }
+}
+
+typedef void (*KernelFn)(const Params);
+KernelFn kernel_nw1(bool sb, bool drop);
+KernelFn kernel_nw2(bool sb, bool drop);
+KernelFn kernel_nw4(bool sb, bool drop);
+KernelFn kernel_nw8(bool sb, bool drop);
+KernelFn kernel_nw16(bool sb, bool drop);
 
 }  // namespace icsched

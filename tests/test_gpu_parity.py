@@ -207,3 +207,28 @@ def test_full_size_sampled(name, sample):
     assert_parity(picked, ref, f"{name} sampled")
     assert got["stats"][0] == B
     assert got["stats"][6] == got["conf_micro"].sum() and got["stats"][7] == got["q_total"].sum()
+
+
+@pytest.mark.parametrize("env", [{"IC_SCHED_NW": "1"}, {"IC_SCHED_NW": "2", "IC_SCHED_DEC": "global"},
+                                 {"IC_SCHED_NW": "4"}, {"IC_SCHED_NW": "8", "IC_SCHED_DEC": "global"},
+                                 {"IC_SCHED_NW": "16"}, {"IC_SCHED_SB": "1", "IC_SCHED_NW": "8"},
+                                 {"IC_SCHED_SB": "1", "IC_SCHED_NW": "16", "IC_SCHED_DEC": "global"},
+                                 {"IC_SCHED_PAD": "32"}, {"IC_SCHED_SLOTS": "1", "IC_SCHED_NW": "2"},
+                                 {"IC_SCHED_SLOTS": "1", "IC_SCHED_SB": "1", "IC_SCHED_NW": "8"}])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_every_kernel_variant(monkeypatch, env, mode):
+    """Every compiled (DP warps, in-place rows, drop mode, decision placement) variant agrees."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(11 + mode)
+    parts = [gen.generate("C3", 40)]
+    tiny = gen.tiny_random(rng, 400, max_tasks=6, max_opt=8, horizon=4096)
+    tiny.deadline[:] = np.where(tiny.deadline >= 0, tiny.deadline * 170 % 4096, tiny.deadline)
+    tiny.mand_wcet[:] = tiny.mand_wcet * 37
+    tiny.opt_wcet[:] = tiny.opt_wcet * 29
+    parts.append(tiny)
+    batch = gen.concat(parts, 8)
+    ocfg = OracleConfig(drop_mode=mode, epsilon_micro=100_000, max_tasks=64, max_horizon=4096)
+    ref = oracle.solve(batch, ocfg, TIME)
+    got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode)
+    assert_parity(got, ref, f"variant {env} mode={mode}")
