@@ -36,10 +36,11 @@ struct Layout {
   int bytes, nq, kp, r1, np2, pad, rs, nbuf;
   int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
       off_sS, off_key;
-  int nslots;
+  int nslots, ndec;
 };
 
-Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_smem, int nslots = 2) {
+Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_smem, int nslots = 2,
+                   int ndec = 1) {
   Layout L{};
   const int nt = 32 * nw;
   const int cols = (c.max_horizon + nt - 1) / nt;
@@ -58,7 +59,8 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
   const int ns = nslots;
   int o = 0;
   L.off_rowbuf = o; o = align16(o + L.nbuf * L.rs * 4);
-  L.off_dec = o;    if (dec_smem) o = align16(o + mt * L.nq * nt * 4);
+  L.off_dec = o;    if (dec_smem) o = align16(o + ndec * mt * L.nq * nt * 4);
+  L.ndec = ndec;
   L.off_rowp = o;   o = align16(o + ns * mt * L.kp * 8);
   L.off_info = o;   o = align16(o + ns * mt * 16);
   L.off_tR = o;     o = align16(o + ns * mt * L.r1 * 4);
@@ -134,13 +136,18 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
     Lg = make_layout(c, nw, sb, pad, false, 1);
   }
   if (Lg.bytes > kSmemLimit) return IC_ERR_LIMIT;
-  Layout Ls = make_layout(c, nw, sb, pad, true, nslots);
-  // decisions in shared memory when that still leaves >= 2 CTAs per SM (IC_SCHED_DEC overrides)
-  bool dec_smem = Ls.bytes <= kSmemLimit / 2;
+  // decisions: a global (L2-resident) double buffer by default, so the backtrack of
+  // instance b overlaps the sweep of b+1; IC_SCHED_DEC=smem keeps one buffer in smem.
+  int ndec = nslots == 2 ? 2 : 1;
+  bool dec_smem = false;
   const char* env = getenv("IC_SCHED_DEC");
-  if (env && !strcmp(env, "smem")) dec_smem = Ls.bytes <= kSmemLimit;
-  if (env && !strcmp(env, "global")) dec_smem = false;
-  const Layout L = dec_smem ? Ls : Lg;
+  if (env && !strcmp(env, "smem")) {
+    Layout Ls = make_layout(c, nw, sb, pad, true, nslots, 1);
+    dec_smem = Ls.bytes <= kSmemLimit;
+    if (dec_smem) ndec = 1;
+  }
+  if (env && !strcmp(env, "global1")) ndec = 1;
+  const Layout L = make_layout(c, nw, sb, pad, dec_smem, nslots, ndec);
 
   KernelFn fn = kernel_for(nw, sb, drop);
   if (!fn) return IC_ERR_LIMIT;
@@ -164,7 +171,7 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   h->ctas_per_sm = per_sm;
   h->grid = sms * per_sm;
   if (!dec_smem) {
-    h->dec_slab_words = (int64_t)c.max_tasks * L.nq * 32 * nw;
+    h->dec_slab_words = (int64_t)c.max_tasks * L.nq * 32 * nw * L.ndec;
     if (cudaMalloc(&h->dec_global, (size_t)h->dec_slab_words * 4 * h->grid) != cudaSuccess) {
       free(h);
       return IC_ERR_OOM;
@@ -266,6 +273,8 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   p.off_key = L.off_key;
   p.rowbuf_stride = L.rs;
   p.nslots = L.nslots;
+  p.ndec = L.ndec;
+  p.dec_words = (int64_t)h->cfg.max_tasks * L.nq * 32 * h->nw;
   int64_t grid = h->grid;
   if (grid > in->n_instances) grid = in->n_instances;
   h->fn<<<(unsigned)grid, 32 * (h->nw + 1), h->L.bytes, (cudaStream_t)cuda_stream>>>(p);

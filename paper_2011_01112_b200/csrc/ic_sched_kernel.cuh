@@ -58,6 +58,8 @@ struct Params {
   int dec_smem;
   uint32_t* dec_global;
   int64_t dec_slab_words;
+  int ndec;            // decision buffers: 2 = the backtrack of b overlaps the sweep of b+1
+  int64_t dec_words;   // words per decision buffer
   // shared-memory layout (byte offsets); slot arrays are [2][...]
   int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
       off_sS, off_key;
@@ -114,17 +116,21 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     return v;
   };
   if (!SB) {
+    constexpr int BATCH = (KK <= 6) ? 8 : 4;  // cells whose loads are in flight together
     for (int g0 = 0; g0 < ng; g0 += 8) {
       const int tb = g0 * NT + tid;
       uint32_t dw = 0;
       if (g0 + 8 <= ng) {
-        int v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = cell(tb + u * NT);
+        for (int h = 0; h < 8; h += BATCH) {
+          int v[BATCH];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          dw |= (uint32_t)(v[u] & 15) << (4 * u);
-          nxt[tb + u * NT] = v[u] | 15;
+          for (int u = 0; u < BATCH; ++u) v[u] = cell(tb + (h + u) * NT);
+#pragma unroll
+          for (int u = 0; u < BATCH; ++u) {
+            dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
+            nxt[tb + (h + u) * NT] = v[u] | 15;
+          }
         }
       } else {
 #pragma unroll
@@ -234,15 +240,22 @@ __device__ __forceinline__ void write_dropped(const Params& p, int64_t b, int64_
   }
 }
 
-// Load task t's optional WCETs and gains (up to KMAX-1, predicated on S).
-__device__ __forceinline__ void load_opt(const Params& p, int64_t t, int Sn, int (&w)[KMAX - 1],
-                                         int (&g)[KMAX - 1]) {
+// Visit task t's optional stages k = 1..Sn with (wcet, gain), loading them in
+// batches of 4 independent loads (the tail warp's register budget is small).
+template <typename F>
+__device__ __forceinline__ void for_each_opt(const Params& p, int64_t t, int Sn, F&& f) {
+  for (int k0 = 0; k0 < Sn; k0 += 4) {
+    int w[4], g[4];
 #pragma unroll
-  for (int k = 0; k < KMAX - 1; ++k) {
-    if (k < Sn) {
-      w[k] = p.opt_wcet[t * p.smax + k];
-      g[k] = p.opt_gain[t * p.smax + k];
+    for (int u = 0; u < 4; ++u) {
+      if (k0 + u < Sn) {
+        w[u] = p.opt_wcet[t * p.smax + k0 + u];
+        g[u] = p.opt_gain[t * p.smax + k0 + u];
+      }
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (k0 + u < Sn) f(k0 + u + 1, w[u], g[u]);
   }
 }
 
@@ -278,20 +291,15 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     S.sr[i] = r;
     S.sS[i] = Sn;
     if (!tb) {
-      int w[KMAX - 1], g[KMAX - 1];
-      load_opt(p, t, Sn, w, g);
       long long C = m, R = a0;
       if ((long long)r + C <= d && R > rmax) rmax = (int)R;
-#pragma unroll
-      for (int k = 0; k < KMAX - 1; ++k) {
-        if (k < Sn) {
-          tb |= (w[k] < 1);
-          C += w[k];
-          R += g[k];
-          tb |= (R < 0) | (R > 1000000);
-          if ((long long)r + C <= d && R > rmax) rmax = (int)R;
-        }
-      }
+      for_each_opt(p, t, Sn, [&](int, int w, int g) {
+        tb |= (w < 1);
+        C += w;
+        R += g;
+        tb |= (R < 0) | (R > 1000000);
+        if ((long long)r + C <= d && R > rmax) rmax = (int)R;
+      });
     }
     bad |= tb;
     const uint32_t dk = (uint32_t)d ^ 0x80000000u;
@@ -343,29 +351,26 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     const int tk = (int)(S.key[pos] & 0xFFF);
     const int64_t t = lo + tk;
     const int d = S.sd[tk], r = S.sr[tk], Sn = S.sS[tk];
-    int w[KMAX - 1], g[KMAX - 1];
-    load_opt(p, t, Sn, w, g);
     int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
     int32_t* trp = S.tR + ((size_t)s * p.max_tasks + pos) * p.r1;
     long long C = p.mand_wcet[t], R = p.mand_conf[t];
     int K = 0, qmax = 0, clast = 0;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      if (k <= Sn) {
-        if (k > 0) {
-          C += w[k - 1];
-          R += g[k - 1];
-        }
-        const int q = (int)(R / delta);
-        qmax = max(qmax, q);
-        if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
-          rp[k] = make_int2((int)C, (q << 4) - (k + 1));
-          trp[k] = (int)R;
-          K = k + 1;
-          clast = (int)C;
-        }
+    auto option = [&](int k) {
+      const int q = (int)(R / delta);
+      qmax = max(qmax, q);
+      if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
+        rp[k] = make_int2((int)C, (q << 4) - (k + 1));
+        trp[k] = (int)R;
+        K = k + 1;
+        clast = (int)C;
       }
-    }
+    };
+    option(0);
+    for_each_opt(p, t, Sn, [&](int k, int w, int g) {
+      C += w;
+      R += g;
+      option(k);
+    });
     qsum += qmax;
     const bool gen = (r > 0) || (K > 0 && clast > p.pad);
     const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
@@ -395,7 +400,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
 
 // a6: backtrack from (Q*, t*) through the decision nibbles (one lane).
 template <int NW>
-__device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, int s, int lane) {
+__device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, int s, int lane, int db) {
   constexpr int NT = 32 * NW;
   const long long* mi = S.misc + s * 16;
   const int n = (int)mi[0];
@@ -411,7 +416,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
           nib = S.tail[s * p.max_tasks + pos];
         } else {
           const int g = t / NT, l = t - g * NT;
-          const uint32_t w = S.dec[((size_t)pos * p.nq + (g >> 3)) * NT + l];
+          const uint32_t w = S.dec[db * p.dec_words + ((size_t)pos * p.nq + (g >> 3)) * NT + l];
           nib = (int)((w >> (4 * (g & 7))) & 15u);
         }
         const int code = 15 - nib;
@@ -506,8 +511,11 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
 }
 
 // ---------------------------------------------------------------------------
+// Resident CTAs per SM the register budget is sized for (85/113/102/113/120 registers).
+constexpr int min_blocks(int nw) { return nw == 1 ? 12 : nw == 2 ? 6 : nw == 4 ? 4 : nw == 8 ? 2 : 1; }
+
 template <int NW, bool SB, bool DROP>
-__global__ void __launch_bounds__(32 * (NW + 1)) ic_dp_kernel(const Params p) {
+__global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(const Params p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NT = 32 * NW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -542,13 +550,19 @@ __global__ void __launch_bounds__(32 * (NW + 1)) ic_dp_kernel(const Params p) {
       int it = 0;
       while (b < p.B) {
         const int s = it & 1;
+        const int db = p.ndec == 2 ? s : 0;
         int64_t nb = b + gridDim.x;
         while (nb < p.B && tail_setup<NW>(p, S, nb, s ^ 1, lane, acc) != ST_OK) nb += gridDim.x;
         if (nb >= p.B && lane == 0) S.misc[(s ^ 1) * 16 + 3] = ST_END;
         __syncwarp();
         bar_sync(BAR_DONE, NT + 32);  // the DP warps finished instance b
-        tail_backtrack<NW>(p, S, s, lane);
-        bar_arrive(BAR_READY, NT + 32);  // decisions free: the DP warps may start nb
+        if (p.ndec == 2) {
+          bar_arrive(BAR_READY, NT + 32);  // nb sweeps into the other decision buffer
+          tail_backtrack<NW>(p, S, s, lane, db);
+        } else {
+          tail_backtrack<NW>(p, S, s, lane, db);
+          bar_arrive(BAR_READY, NT + 32);  // decisions free: the DP warps may start nb
+        }
         tail_outputs(p, S, s, lane, acc);
         b = nb;
         ++it;
@@ -556,7 +570,7 @@ __global__ void __launch_bounds__(32 * (NW + 1)) ic_dp_kernel(const Params p) {
     } else {
       while (b < p.B) {
         bar_sync(BAR_DONE, NT + 32);
-        tail_backtrack<NW>(p, S, 0, lane);
+        tail_backtrack<NW>(p, S, 0, lane, 0);
         tail_outputs(p, S, 0, lane, acc);
         int64_t nb = b + gridDim.x;
         while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb += gridDim.x;
@@ -580,6 +594,7 @@ __global__ void __launch_bounds__(32 * (NW + 1)) ic_dp_kernel(const Params p) {
   for (int it = 0;; ++it) {
     bar_sync(BAR_READY, NT + 32);
     const int s = p.nslots == 2 ? (it & 1) : 0;
+    uint32_t* decb = S.dec + (p.ndec == 2 && p.nslots == 2 ? (it & 1) : 0) * p.dec_words;
     long long* mi = S.misc + s * 16;
     if (mi[3] == ST_END) break;
     const int n = (int)mi[0];
@@ -607,7 +622,7 @@ __global__ void __launch_bounds__(32 * (NW + 1)) ic_dp_kernel(const Params p) {
       const int Mv = DROP ? max(M, A) : A;
       if (tid == 0) S.tail[s * p.max_tasks + pos] = Mv & 15;
       const int Mn = Mv | 15;
-      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, S.dec + (size_t)pos * p.nq * NT,
+      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, decb + (size_t)pos * p.nq * NT,
                                     (const int4*)ops, d, r, p.nq);
       // G_pos(t) = M_pos on (d, d_next]: the next row reads it there
       if (pos + 1 < n) {
