@@ -131,18 +131,28 @@ def workload_config(cw, args, n_instances):
             "horizon": cw.horizon, "seed": hex(cw.seed)}
 
 
+def _calibrate_oracle(cw, ocfg, threads, target_s):
+    """Instances of `cw` the oracle solves in about target_s seconds on `threads` threads."""
+    import oracle
+    n = max(threads * 4, 32)
+    while True:
+        sample = gen.generate(cw, n, id_offset=1 << 30)
+        t0 = time.perf_counter()
+        oracle.solve(sample, ocfg, oracle.PAPER, threads)
+        dt = time.perf_counter() - t0
+        if dt >= 1.0 or n >= cw.n_instances:
+            return int(min(cw.n_instances, max(threads, n * target_s / max(dt, 1e-6))))
+        n *= 4
+
+
 def cpu_oracle_rate(cw, args, target_s):
     """The oracle as it stands (paper DP, OpenMP over instances) on a bounded sample."""
     import oracle
     threads = os.cpu_count() or 1
     ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
                                max_tasks=cw.n_tasks, max_horizon=cw.horizon)
-    probe = gen.generate(cw, max(threads * 2, 16))
-    t0 = time.perf_counter()
-    oracle.solve(probe, ocfg, oracle.PAPER, threads)
-    dt = max(time.perf_counter() - t0, 1e-4)
-    n = int(min(cw.n_instances, max(probe.n_instances, probe.n_instances * target_s / dt)))
-    sample = gen.generate(cw, n, id_offset=probe.n_instances)
+    n = _calibrate_oracle(cw, ocfg, threads, target_s)
+    sample = gen.generate(cw, n)
     t0 = time.perf_counter()
     oracle.solve(sample, ocfg, oracle.PAPER, threads)
     el = time.perf_counter() - t0
@@ -157,12 +167,8 @@ def run_reference(args, cw, rank, world):
     threads = os.cpu_count() or 1
     ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
                                max_tasks=cw.n_tasks, max_horizon=cw.horizon)
-    # size each step for ~3 s of CPU work so K+W steps stay within a few minutes
-    probe = gen.generate(cw, max(threads * 2, 16))
-    t0 = time.perf_counter()
-    oracle.solve(probe, ocfg, oracle.PAPER, threads)
-    per = max(time.perf_counter() - t0, 1e-4) / probe.n_instances
-    n = int(min(cw.n_instances, max(threads, 3.0 / per)))
+    # size each step for ~10 s of CPU work so K+W steps stay within a few minutes
+    n = _calibrate_oracle(cw, ocfg, threads, 10.0)
     sample = gen.generate(cw, n)
     for _ in range(args.warmup):
         oracle.solve(sample, ocfg, oracle.PAPER, threads)
@@ -360,8 +366,8 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             v, n, el, thr = cpu_oracle_rate(cw, args, args.cpu_seconds)
             line["cpu_baseline"] = {"value": v, "unit": "instances/s", "cores": thr, "kind": "oracle",
-                                    "sample": f"{n} {cw.name} instances (ids after the probe), paper "
-                                              f"reward-indexed DP (O2), {el:.1f} s"}
+                                    "sample": f"{n} {cw.name} instances (ids 0..{n - 1}), paper "
+                                              f"reward-indexed DP (O2) on {thr} OpenMP threads, {el:.1f} s"}
         print(json.dumps(line), flush=True)
     sched.close()
     if world > 1:

@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace icsched {
 
 constexpr int NEG = -(1 << 30);
@@ -133,14 +135,24 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
           }
         }
       } else {
+        // ragged last chunk: 4 + 2 + 1 groups, each sub-batch issuing its loads together
+        const int rem = ng - g0;
+        int u0 = 0;
+        auto sub = [&](auto nb_tag) {
+          constexpr int NB = decltype(nb_tag)::value;
+          int v[NB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (g0 + u < ng) {
-            const int v = cell(tb + u * NT);
-            dw |= (uint32_t)(v & 15) << (4 * u);
-            nxt[tb + u * NT] = v | 15;
+          for (int u = 0; u < NB; ++u) v[u] = cell(tb + (u0 + u) * NT);
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            dw |= (uint32_t)(v[u] & 15) << (4 * (u0 + u));
+            nxt[tb + (u0 + u) * NT] = v[u] | 15;
           }
-        }
+          u0 += NB;
+        };
+        if (rem & 4) sub(std::integral_constant<int, 4>{});
+        if (rem & 2) sub(std::integral_constant<int, 2>{});
+        if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
       decrow[(g0 >> 3) * NT + tid] = dw;
     }
@@ -604,33 +616,44 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     const int4* inf = S.info + s * p.max_tasks;
     const int2* rpb = S.rowp + (size_t)s * p.max_tasks * p.kp;
     int M = 15;
+    int4 f = inf[0];
+    int32_t* const tailp = S.tail + s * p.max_tasks;
+    const int2* ops = rpb;
+    uint32_t* decrow = decb;
+    const size_t dec_row_words = (size_t)p.nq * NT;
+    const int kp = p.kp;
+#pragma unroll 1
     for (int pos = 0; pos < n; ++pos) {
-      const int4 f = inf[pos];
+      const int4 fn = pos + 1 < n ? inf[pos + 1] : f;  // next row's header, off the critical path
       const int d = f.x, K = f.y & 255, r = f.z, dn = f.w;
       const bool gen = (f.y >> 8) & 1;
       const int32_t* cur = buf0 + (pos & 1) * RSb;
       int32_t* nxt = buf0 + ((pos + 1) & 1) * RSb;
-      const int2* ops = rpb + (size_t)pos * p.kp;
-      // admit value at column d: every column t > d shares it (tail collapse)
+      // admit value at column d: every column t > d shares it (tail collapse).  In
+      // double-buffered mode its loads are issued here and consumed after the sweep.
       int av = NEG;
       if (lane < K) {
         const int2 o = ops[lane];
         const int src = d - o.x;
         if (src >= r) av = cur[src] + o.y;
       }
-      const int A = __reduce_max_sync(0xffffffffu, av);
+      int A = 0;
+      if (SB) A = __reduce_max_sync(0xffffffffu, av);
+      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, p.nq);
+      if (!SB) A = __reduce_max_sync(0xffffffffu, av);
       const int Mv = DROP ? max(M, A) : A;
-      if (tid == 0) S.tail[s * p.max_tasks + pos] = Mv & 15;
+      if (tid == 0) tailp[pos] = Mv & 15;
       const int Mn = Mv | 15;
-      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, decb + (size_t)pos * p.nq * NT,
-                                    (const int4*)ops, d, r, p.nq);
       // G_pos(t) = M_pos on (d, d_next]: the next row reads it there
-      if (pos + 1 < n) {
+      if (dn > d) {
         const int first = d + 1 > 0 ? d + 1 : 0;
-        int t = first + ((tid - first) % NT + NT) % NT;
-        for (; t <= dn; t += NT) nxt[t] = Mn;
+#pragma unroll 1
+        for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = Mn;
       }
       M = Mn;
+      f = fn;
+      ops += kp;
+      decrow += dec_row_words;
       bar_sync(BAR_DP, NT);
     }
     // a5: Q* = G_N(T), t* = least t with G_N(t) = Q*  (G_N non-decreasing on [0, d_N])
