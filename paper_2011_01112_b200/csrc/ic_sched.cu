@@ -87,8 +87,11 @@ struct ic_sched {
   int dec_smem, sms, ctas_per_sm, grid;
   uint32_t* dec_global;
   int64_t dec_slab_words;
+  unsigned long long* work;
   void* stage;
   size_t stage_bytes;
+  cudaStream_t s_in, s_comp, s_out;  // host entry point: copy-in / compute / copy-out pipeline
+  cudaEvent_t ev[3 * 16 + 1];
 };
 
 static int env_int(const char* name, int dflt) {
@@ -170,6 +173,10 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   h->sms = sms;
   h->ctas_per_sm = per_sm;
   h->grid = sms * per_sm;
+  if (cudaMalloc(&h->work, 16) != cudaSuccess || cudaMemset(h->work, 0, 16) != cudaSuccess) {
+    free(h);
+    return IC_ERR_OOM;
+  }
   if (!dec_smem) {
     h->dec_slab_words = (int64_t)c.max_tasks * L.nq * 32 * nw * L.ndec;
     if (cudaMalloc(&h->dec_global, (size_t)h->dec_slab_words * 4 * h->grid) != cudaSuccess) {
@@ -185,7 +192,14 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
   if (!h) return IC_ERR_INVALID_ARG;
   cudaSetDevice(h->cfg.device);
   if (h->dec_global) cudaFree(h->dec_global);
+  if (h->work) cudaFree(h->work);
   if (h->stage) cudaFree(h->stage);
+  if (h->s_in) {
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_comp);
+    cudaStreamDestroy(h->s_out);
+    for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  }
   free(h);
   return IC_OK;
 }
@@ -273,6 +287,7 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   p.off_key = L.off_key;
   p.rowbuf_stride = L.rs;
   p.nslots = L.nslots;
+  p.work = h->work;
   p.ndec = L.ndec;
   p.dec_words = (int64_t)h->cfg.max_tasks * L.nq * 32 * h->nw;
   int64_t grid = h->grid;
@@ -282,8 +297,11 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   return IC_OK;
 }
 
-// Host-buffer entry point: H2D of the inputs, solve, D2H of the outputs, all on
-// `cuda_stream`, synchronised before returning.
+// Host-buffer entry point: H2D of the inputs, solve, D2H of the outputs.  The batch
+// is cut into up to 16 instance chunks pipelined over three internal streams
+// (copy-in, compute, copy-out) so PCIe traffic overlaps the sweep; kernels stay
+// serialised on the compute stream (they share the decision workspace).  Ordered
+// after prior work on `cuda_stream`; synchronised before returning.
 extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_batch_out* out,
                                          void* cuda_stream) {
   if (!h) return IC_ERR_INVALID_ARG;
@@ -291,17 +309,21 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
   if (rc != IC_OK) return rc;
   if (in->n_instances == 0) return IC_OK;
   if (cudaSetDevice(h->cfg.device) != cudaSuccess) return IC_ERR_CUDA;
-  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (!h->s_in) {
+    if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->s_comp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking) != cudaSuccess)
+      return IC_ERR_CUDA;
+    for (cudaEvent_t& e : h->ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return IC_ERR_CUDA;
+  }
   const int64_t B = in->n_instances;
-  int64_t first = 0, last = 0;
-  memcpy(&first, in->task_begin, 8);
-  memcpy(&last, in->task_begin + B, 8);
-  if (last < first) return IC_ERR_INVALID_ARG;
-  const int64_t T = last;  // rows [0, last) are addressed by the CSR offsets
+  const int64_t* tbh = in->task_begin;
+  if (tbh[B] < tbh[0]) return IC_ERR_INVALID_ARG;
+  const int64_t T = tbh[B];  // task rows [0, T) are addressed by the CSR offsets
   const int64_t st = h->cfg.max_opt_stages;
-  // staging layout (8-byte aligned pieces)
   size_t off = 0;
-  auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 15) & ~(size_t)15; return o; };
+  auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
   const size_t o_tb = take((B + 1) * 8), o_r = take(T * 4), o_d = take(T * 4), o_m = take(T * 4),
                o_n = take(T), o_ow = take(T * st * 4), o_mc = take(T * 4), o_og = take(T * st * 4),
                o_k = take(T), o_s = take(T * 4), o_f = take(T * 4), o_q = take(B * 8), o_c = take(B * 8),
@@ -314,33 +336,55 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
     h->stage_bytes = off;
   }
   char* g = (char*)h->stage;
-  auto h2d = [&](size_t o, const void* src, size_t bytes) {
-    return bytes == 0 || cudaMemcpyAsync(g + o, src, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
-  };
-  auto d2h = [&](void* dst, size_t o, size_t bytes) {
-    return bytes == 0 || cudaMemcpyAsync(dst, g + o, bytes, cudaMemcpyDeviceToHost, s) == cudaSuccess;
-  };
-  bool ok = h2d(o_tb, in->task_begin, (B + 1) * 8) && h2d(o_r, in->release, T * 4) &&
-            h2d(o_d, in->deadline, T * 4) && h2d(o_m, in->mand_wcet, T * 4) && h2d(o_n, in->n_opt, T) &&
-            h2d(o_mc, in->mand_conf, T * 4);
-  if (st > 0) ok = ok && h2d(o_ow, in->opt_wcet, T * st * 4) && h2d(o_og, in->opt_gain, T * st * 4);
-  if (out->stats) ok = ok && cudaMemsetAsync(g + o_stats, 0, 64, s) == cudaSuccess;
-  if (!ok) return IC_ERR_CUDA;
-  ic_batch_in din = {B, (const int64_t*)(g + o_tb), (const int32_t*)(g + o_r), (const int32_t*)(g + o_d),
-                     (const int32_t*)(g + o_m), (const uint8_t*)(g + o_n), (const int32_t*)(g + o_ow),
-                     (const uint32_t*)(g + o_mc), (const int32_t*)(g + o_og)};
-  ic_batch_out dout = {(int8_t*)(g + o_k), (int32_t*)(g + o_s), (int32_t*)(g + o_f), (int64_t*)(g + o_q),
-                       (int64_t*)(g + o_c), (double*)(g + o_ct), (int32_t*)(g + o_ms), (uint8_t*)(g + o_st),
-                       out->stats ? (int64_t*)(g + o_stats) : nullptr};
-  rc = ic_sched_solve_batch(h, &din, &dout, cuda_stream);
-  if (rc != IC_OK) return rc;
-  ok = d2h(out->kept, o_k, T) && d2h(out->start, o_s, T * 4) && d2h(out->finish, o_f, T * 4) &&
-       d2h(out->q_total, o_q, B * 8) && d2h(out->conf_micro, o_c, B * 8) &&
-       d2h(out->conf_total, o_ct, B * 8) && d2h(out->makespan, o_ms, B * 4) && d2h(out->status, o_st, B);
+  cudaStream_t user = (cudaStream_t)cuda_stream;
+  cudaEvent_t* ev = h->ev;
+  bool ok = cudaEventRecord(ev[48], user) == cudaSuccess &&
+            cudaStreamWaitEvent(h->s_in, ev[48], 0) == cudaSuccess &&
+            cudaStreamWaitEvent(h->s_comp, ev[48], 0) == cudaSuccess;
+  if (out->stats) ok = ok && cudaMemsetAsync(g + o_stats, 0, 64, h->s_comp) == cudaSuccess;
+  const int64_t nch = B >= 16 * 256 ? 16 : (B + 255) / 256;
+  for (int64_t j = 0; j < nch && ok; ++j) {
+    const int64_t b0 = B * j / nch, b1 = B * (j + 1) / nch;
+    const int64_t t0 = tbh[b0], t1 = tbh[b1], nt = t1 - t0;
+    if (t1 < t0) return IC_ERR_INVALID_ARG;
+    cudaEvent_t e_in = ev[(j % 16) * 3], e_k = ev[(j % 16) * 3 + 1];
+    auto h2d = [&](size_t o, const void* src, size_t bytes) {
+      return bytes == 0 || cudaMemcpyAsync(g + o, src, bytes, cudaMemcpyHostToDevice, h->s_in) == cudaSuccess;
+    };
+    ok = h2d(o_tb + b0 * 8, tbh + b0, (b1 - b0 + 1) * 8) && h2d(o_r + t0 * 4, in->release + t0, nt * 4) &&
+         h2d(o_d + t0 * 4, in->deadline + t0, nt * 4) && h2d(o_m + t0 * 4, in->mand_wcet + t0, nt * 4) &&
+         h2d(o_n + t0, in->n_opt + t0, nt) && h2d(o_mc + t0 * 4, in->mand_conf + t0, nt * 4);
+    if (st > 0)
+      ok = ok && h2d(o_ow + t0 * st * 4, in->opt_wcet + t0 * st, nt * st * 4) &&
+           h2d(o_og + t0 * st * 4, in->opt_gain + t0 * st, nt * st * 4);
+    ok = ok && cudaEventRecord(e_in, h->s_in) == cudaSuccess &&
+         cudaStreamWaitEvent(h->s_comp, e_in, 0) == cudaSuccess;
+    if (!ok) break;
+    ic_batch_in din = {b1 - b0, (const int64_t*)(g + o_tb) + b0, (const int32_t*)(g + o_r),
+                       (const int32_t*)(g + o_d), (const int32_t*)(g + o_m), (const uint8_t*)(g + o_n),
+                       (const int32_t*)(g + o_ow), (const uint32_t*)(g + o_mc), (const int32_t*)(g + o_og)};
+    ic_batch_out dout = {(int8_t*)(g + o_k), (int32_t*)(g + o_s), (int32_t*)(g + o_f),
+                         (int64_t*)(g + o_q) + b0, (int64_t*)(g + o_c) + b0, (double*)(g + o_ct) + b0,
+                         (int32_t*)(g + o_ms) + b0, (uint8_t*)(g + o_st) + b0,
+                         out->stats ? (int64_t*)(g + o_stats) : nullptr};
+    rc = ic_sched_solve_batch(h, &din, &dout, h->s_comp);
+    if (rc != IC_OK) return rc;
+    ok = cudaEventRecord(e_k, h->s_comp) == cudaSuccess && cudaStreamWaitEvent(h->s_out, e_k, 0) == cudaSuccess;
+    auto d2h = [&](void* dst, size_t o, size_t bytes) {
+      return bytes == 0 || cudaMemcpyAsync(dst, g + o, bytes, cudaMemcpyDeviceToHost, h->s_out) == cudaSuccess;
+    };
+    ok = ok && d2h(out->kept + t0, o_k + t0, nt) && d2h(out->start + t0, o_s + t0 * 4, nt * 4) &&
+         d2h(out->finish + t0, o_f + t0 * 4, nt * 4) && d2h(out->q_total + b0, o_q + b0 * 8, (b1 - b0) * 8) &&
+         d2h(out->conf_micro + b0, o_c + b0 * 8, (b1 - b0) * 8) &&
+         d2h(out->conf_total + b0, o_ct + b0 * 8, (b1 - b0) * 8) &&
+         d2h(out->makespan + b0, o_ms + b0 * 4, (b1 - b0) * 4) && d2h(out->status + b0, o_st + b0, b1 - b0);
+  }
   int64_t stats_dev[8];
-  if (out->stats) ok = ok && d2h(stats_dev, o_stats, 64);
-  if (!ok) return IC_ERR_CUDA;
-  if (cudaStreamSynchronize(s) != cudaSuccess) return IC_ERR_CUDA;
+  if (ok && out->stats) {
+    ok = cudaEventRecord(ev[47], h->s_comp) == cudaSuccess && cudaStreamWaitEvent(h->s_out, ev[47], 0) == cudaSuccess &&
+         cudaMemcpyAsync(stats_dev, g + o_stats, 64, cudaMemcpyDeviceToHost, h->s_out) == cudaSuccess;
+  }
+  if (cudaStreamSynchronize(h->s_out) != cudaSuccess || !ok) return IC_ERR_CUDA;
   if (out->stats)
     for (int i = 0; i < 8; ++i) out->stats[i] += stats_dev[i];
   return IC_OK;

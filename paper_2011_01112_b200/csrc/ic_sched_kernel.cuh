@@ -66,6 +66,7 @@ struct Params {
   int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
       off_sS, off_key;
   int nslots;  // 2: set up instance b+1 while the DP sweeps b; 1: serialised (large N)
+  unsigned long long* work;  // [2] dynamic instance counter, CTAs finished (reset by the last CTA)
   int rowbuf_stride;  // ints per row buffer (pad + capacity)
 };
 
@@ -553,8 +554,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
   if (warp == NW) {
     // ================= tail warp =================
     unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int64_t b = blockIdx.x;
-    while (b < p.B && tail_setup<NW>(p, S, b, 0, lane, acc) != ST_OK) b += gridDim.x;
+    // instances are claimed dynamically (work varies with U): one atomic per instance
+    auto claim = [&]() -> int64_t {
+      unsigned long long v = 0;
+      if (lane == 0) v = atomicAdd(&p.work[0], 1ull);
+      return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    int64_t b = claim();
+    while (b < p.B && tail_setup<NW>(p, S, b, 0, lane, acc) != ST_OK) b = claim();
     if (b >= p.B && lane == 0) S.misc[3] = ST_END;
     __syncwarp();
     bar_arrive(BAR_READY, NT + 32);
@@ -563,8 +570,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       while (b < p.B) {
         const int s = it & 1;
         const int db = p.ndec == 2 ? s : 0;
-        int64_t nb = b + gridDim.x;
-        while (nb < p.B && tail_setup<NW>(p, S, nb, s ^ 1, lane, acc) != ST_OK) nb += gridDim.x;
+        int64_t nb = claim();
+        while (nb < p.B && tail_setup<NW>(p, S, nb, s ^ 1, lane, acc) != ST_OK) nb = claim();
         if (nb >= p.B && lane == 0) S.misc[(s ^ 1) * 16 + 3] = ST_END;
         __syncwarp();
         bar_sync(BAR_DONE, NT + 32);  // the DP warps finished instance b
@@ -584,8 +591,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         bar_sync(BAR_DONE, NT + 32);
         tail_backtrack<NW>(p, S, 0, lane, 0);
         tail_outputs(p, S, 0, lane, acc);
-        int64_t nb = b + gridDim.x;
-        while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb += gridDim.x;
+        int64_t nb = claim();
+        while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb = claim();
         if (nb >= p.B && lane == 0) S.misc[3] = ST_END;
         __syncwarp();
         bar_arrive(BAR_READY, NT + 32);
@@ -596,6 +603,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (acc[i]) atomicAdd(&p.stats[i], acc[i]);
+    }
+    if (lane == 0) {  // the last CTA out resets the counters for the next launch
+      __threadfence();
+      if (atomicAdd(&p.work[1], 1ull) == gridDim.x - 1) {
+        p.work[0] = 0;
+        p.work[1] = 0;
+      }
     }
     return;
   }
