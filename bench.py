@@ -337,7 +337,7 @@ def main():
         prof = os.path.join(ROOT, "profiles", f"ncu_{cw.name}_summary.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+                traffic = json.load(open(prof)).get("dram_bytes_per_instance") * n_inst
             except Exception:
                 traffic = None
         line = {
