@@ -141,19 +141,21 @@ class Batch:
 
 
 def concat(parts, stride: int) -> Batch:
+    """Concatenate batches (each may hold any number of instances) into one."""
     parts = [p.with_stride(stride) for p in parts]
-    sizes = [p.n_total_tasks for p in parts]
-    tb = np.zeros(len(parts) + 1, np.int64)
-    tb[1:] = np.cumsum(sizes)
-    cat = lambda f: np.concatenate([getattr(p, f) for p in parts]) if parts else None
+    tbs, base = [np.zeros(1, np.int64)], 0
+    for p in parts:
+        tbs.append(p.task_begin[1:] - p.task_begin[0] + base)
+        base += p.n_total_tasks
+    tb = np.concatenate(tbs).astype(np.int64)
     if not parts:
         e = np.zeros(0, np.int32)
         return Batch(tb, e, e, e, np.zeros(0, np.uint8), np.zeros((0, stride), np.int32),
                      np.zeros(0, np.uint32), np.zeros((0, stride), np.int32))
+    cat = lambda f: np.concatenate([getattr(p, f)[int(p.task_begin[0]):int(p.task_begin[-1])] for p in parts])
     return Batch(tb, cat("release"), cat("deadline"), cat("mand_wcet"), cat("n_opt"),
-                 np.concatenate([p.opt_wcet for p in parts]).reshape(int(tb[-1]), stride),
-                 cat("mand_conf"),
-                 np.concatenate([p.opt_gain for p in parts]).reshape(int(tb[-1]), stride))
+                 cat("opt_wcet").reshape(int(tb[-1]), stride), cat("mand_conf"),
+                 cat("opt_gain").reshape(int(tb[-1]), stride))
 
 
 def build(force: bool = False) -> str:

@@ -19,5 +19,5 @@ from .abi import (  # noqa: F401
     IC_INST_OK, IC_INST_INFEASIBLE, IC_INST_BAD_INPUT, IC_INST_LIMIT,
     INPUT_FIELDS, OUTPUT_FIELDS, STATS_FIELDS,
     SchedConfig, SchedInfo, Scheduler, ICSchedError, lib_path, load_library,
-    alloc_outputs, gen_batch_device,
+    alloc_inputs, alloc_outputs, gen_batch_device,
 )

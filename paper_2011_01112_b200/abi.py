@@ -203,16 +203,26 @@ class Scheduler:
         self.close()
 
 
+def alloc_inputs(n_instances: int, n_tasks_total: int, opt_stride: int, device="cuda") -> dict:
+    """Empty input buffers in the ABI layout on a CUDA device."""
+    import torch
+    B, T = int(n_instances), int(n_tasks_total)
+    return {n: torch.empty((T, opt_stride) if k == "task_opt" else (B + 1 if k == "csr" else T),
+                           dtype=torch.from_numpy(np.zeros(0, dt)).dtype, device=torch.device(device))
+            for n, dt, k in INPUT_FIELDS}
+
+
 def gen_batch_device(seed, n_tasks, n_opt, opt_stride, horizon, u_lo_q16, u_hi_q16, d_lo, n_instances,
-                     id_offset=0, release_mode=0, device="cuda", stream=None) -> dict:
-    """ic_gen_batch_device: generate instances [id_offset, id_offset+n) on the GPU (ABI layout)."""
+                     id_offset=0, release_mode=0, device="cuda", stream=None, out: dict | None = None) -> dict:
+    """ic_gen_batch_device: generate instances [id_offset, id_offset+n) on the GPU (ABI layout).
+
+    With ``out`` (tensors or views of at least the batch's size) the rows are written there;
+    its task_begin then holds offsets relative to the first generated row."""
     import torch
     lib = load_library()
     B, T = int(n_instances), int(n_instances) * int(n_tasks)
     dev = torch.device(device)
-    t = {n: torch.empty((T, opt_stride) if k == "task_opt" else (B + 1 if k == "csr" else T),
-                        dtype=torch.from_numpy(np.zeros(0, dt)).dtype, device=dev)
-         for n, dt, k in INPUT_FIELDS}
+    t = out if out is not None else alloc_inputs(B, T, opt_stride, dev)
     g = _GenCfg(seed, n_tasks, n_opt, opt_stride, horizon, u_lo_q16, u_hi_q16, d_lo, release_mode)
     if stream is None:
         stream = torch.cuda.current_stream(dev)

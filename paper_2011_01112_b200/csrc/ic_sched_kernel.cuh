@@ -84,7 +84,7 @@ __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax
 template <int NW, bool SB, bool DROP, int K, bool GEN>
 __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
                                        const int4* __restrict__ ops4, const int d, const int r, const int kr,
-                                       const int nq) {
+                                       const int pad) {
   constexpr int NT = 32 * NW;
   constexpr int KK = GEN ? KMAX : K;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -103,15 +103,21 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   }
   const int w0 = warp * 32;
   const int ng = d >= w0 ? (d - w0) / NT + 1 : 0;  // this warp's groups holding a column t <= d
-  auto cell = [&](int t) -> int {
+  // groups whose longest option reaches left of the NEG pad read through a clamp
+  const int reach = (!GEN && KK > 0) ? C[KK > 0 ? KK - 1 : 0] - pad - w0 : 0;
+  const int gcl = GEN ? ng : (reach > 0 ? (reach + NT - 1) / NT : 0);
+  auto cell = [&](int t, auto clamp_tag) -> int {
+    constexpr bool CL = decltype(clamp_tag)::value;
     int v = DROP ? cur[t] : NEG;
 #pragma unroll
     for (int k = 0; k < KK; ++k) {
-      if (GEN) {
+      if (GEN) {  // releases: options with a source before r are invalid (read a NEG cell)
         if (k < kr) {
           const int src = t - C[k];
-          if (src >= r) v = viaddmax(cur[src], key[k], v);
+          v = viaddmax(cur[src >= r ? src : -1], key[k], v);
         }
+      } else if (CL) {
+        v = viaddmax(cur[max(t - C[k], -pad)], key[k], v);
       } else {
         v = viaddmax(cur[t - C[k]], key[k], v);
       }
@@ -120,7 +126,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   };
   if (!SB) {
     constexpr int BATCH = (KK <= 6) ? 8 : 4;  // cells whose loads are in flight together
-    for (int g0 = 0; g0 < ng; g0 += 8) {
+    auto chunk = [&](int g0, auto clamp_tag) {
       const int tb = g0 * NT + tid;
       uint32_t dw = 0;
       if (g0 + 8 <= ng) {
@@ -128,7 +134,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         for (int h = 0; h < 8; h += BATCH) {
           int v[BATCH];
 #pragma unroll
-          for (int u = 0; u < BATCH; ++u) v[u] = cell(tb + (h + u) * NT);
+          for (int u = 0; u < BATCH; ++u) v[u] = cell(tb + (h + u) * NT, clamp_tag);
 #pragma unroll
           for (int u = 0; u < BATCH; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
@@ -143,7 +149,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
           constexpr int NB = decltype(nb_tag)::value;
           int v[NB];
 #pragma unroll
-          for (int u = 0; u < NB; ++u) v[u] = cell(tb + (u0 + u) * NT);
+          for (int u = 0; u < NB; ++u) v[u] = cell(tb + (u0 + u) * NT, clamp_tag);
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (u0 + u));
@@ -156,7 +162,11 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
       decrow[(g0 >> 3) * NT + tid] = dw;
-    }
+    };
+    int g0 = 0;
+    if (gcl > 0)  // rare: options longer than the pad
+      for (; g0 < ng && g0 < gcl; g0 += 8) chunk(g0, std::true_type{});
+    for (; g0 < ng; g0 += 8) chunk(g0, std::false_type{});
   } else {
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
     // chunk c reads only columns below its top, so writing it after the barrier
@@ -166,8 +176,13 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       const int g0 = c * 8;
       const int tb = g0 * NT + tid;
       int v[8];
+      if (g0 < gcl) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT) : 0;
+        for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::true_type{}) : 0;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::false_type{}) : 0;
+      }
       bar_sync(BAR_DP, NT);
       uint32_t dw = 0;
 #pragma unroll
@@ -180,18 +195,17 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       if (g0 < ng) decrow[(g0 >> 3) * NT + tid] = dw;
     }
   }
-  (void)nq;
 }
 
 template <int NW, bool SB, bool DROP>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
-                                                uint32_t* decrow, const int4* ops4, int d, int r, int nq) {
+                                                uint32_t* decrow, const int4* ops4, int d, int r, int pad) {
   if (gen) {
-    dp_row<NW, SB, DROP, KMAX, true>(cur, nxt, decrow, ops4, d, r, K, nq);
+    dp_row<NW, SB, DROP, KMAX, true>(cur, nxt, decrow, ops4, d, r, K, pad);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: dp_row<NW, SB, DROP, KK, false>(cur, nxt, decrow, ops4, d, r, K, nq); break;
+  case KK: dp_row<NW, SB, DROP, KK, false>(cur, nxt, decrow, ops4, d, r, K, pad); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -367,7 +381,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
     int32_t* trp = S.tR + ((size_t)s * p.max_tasks + pos) * p.r1;
     long long C = p.mand_wcet[t], R = p.mand_conf[t];
-    int K = 0, qmax = 0, clast = 0;
+    int K = 0, qmax = 0;
     auto option = [&](int k) {
       const int q = (int)(R / delta);
       qmax = max(qmax, q);
@@ -375,7 +389,6 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
         rp[k] = make_int2((int)C, (q << 4) - (k + 1));
         trp[k] = (int)R;
         K = k + 1;
-        clast = (int)C;
       }
     };
     option(0);
@@ -385,7 +398,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       option(k);
     });
     qsum += qmax;
-    const bool gen = (r > 0) || (K > 0 && clast > p.pad);
+    const bool gen = r > 0;  // releases take the masked path; long options clamp per group
     const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
     S.info[s * p.max_tasks + pos] = make_int4(d, K | (gen ? 256 : 0) | (Sn << 16), r, dn);
     S.task[s * p.max_tasks + pos] = tk;
@@ -653,7 +666,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       }
       int A = 0;
       if (SB) A = __reduce_max_sync(0xffffffffu, av);
-      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, p.nq);
+      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, p.pad);
       if (!SB) A = __reduce_max_sync(0xffffffffu, av);
       const int Mv = DROP ? max(M, A) : A;
       if (tid == 0) tailp[pos] = Mv & 15;

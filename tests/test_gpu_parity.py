@@ -178,7 +178,7 @@ def test_decisions_in_global_memory(monkeypatch):
     assert_parity(got, ref, "global decisions")
 
 
-@pytest.mark.parametrize("name,sample", [("C2", 97), ("C3", 2003)])
+@pytest.mark.parametrize("name,sample", [("C2", 97), ("C3", 2003), ("C4", 2503)])
 def test_full_size_sampled(name, sample):
     """BASELINE.json full sizes in the bench launch configuration (device-generated inputs);
     a deterministic sample is checked element by element against the oracle, every instance by
@@ -232,3 +232,19 @@ def test_every_kernel_variant(monkeypatch, env, mode):
     ref = oracle.solve(batch, ocfg, TIME)
     got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode)
     assert_parity(got, ref, f"variant {env} mode={mode}")
+
+
+def test_c5_sweep_blocks():
+    """C5's utilisation blocks (U = 1, 2, 4, 8): instances straddling every block boundary."""
+    cw = gen.CONFIGS["C5"]
+    parts = [gen.generate(cw, 24, id_offset=(k << 22) - 12) for k in (1, 2, 3)]
+    parts.append(gen.generate(cw, 12, id_offset=(4 << 22) - 12))
+    batch = gen.concat(parts, cw.n_opt)
+    ocfg = OracleConfig(epsilon_micro=cw.epsilon_micro, max_tasks=cw.n_tasks, max_horizon=cw.horizon)
+    ref = oracle.solve(batch, ocfg, TIME)
+    got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon)
+    assert_parity(got, ref, "C5 blocks")
+    # overload shows up as planned misses only at the high-U blocks (SURVEY Appendix A3)
+    tb = batch.task_begin
+    drops = [(got["kept"][tb[b]:tb[b + 1]] < 0).mean() for b in range(batch.n_instances)]
+    assert np.mean(drops[-12:]) > np.mean(drops[:12])
