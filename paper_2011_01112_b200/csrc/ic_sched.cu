@@ -121,7 +121,8 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   if (nw != 1 && nw != 2 && nw != 4 && nw != 8 && nw != 16) return IC_ERR_INVALID_ARG;
   // NEG pad left of column 0: rows whose longest usable option reaches further use
   // the masked general path, so the pad only trades shared memory for speed.
-  int pad = c.max_horizon < 256 ? c.max_horizon : 256;
+  int pad = c.max_horizon / 16 < 64 ? 64 : (c.max_horizon / 16 > 256 ? 256 : c.max_horizon / 16);
+  if (pad > c.max_horizon) pad = c.max_horizon;
   pad = env_int("IC_SCHED_PAD", pad);
   pad = (pad + 31) & ~31;
 

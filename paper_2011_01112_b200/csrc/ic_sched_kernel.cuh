@@ -176,7 +176,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       const int g0 = c * 8;
       const int tb = g0 * NT + tid;
       int v[8];
-      if (g0 < gcl) {
+      if (gcl > 0 && g0 < gcl) {  // rare: options longer than the pad
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::true_type{}) : 0;
       } else {
