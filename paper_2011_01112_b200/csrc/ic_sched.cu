@@ -61,7 +61,7 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
   L.off_rowbuf = o; o = align16(o + L.nbuf * L.rs * 4);
   L.off_dec = o;    if (dec_smem) o = align16(o + ndec * mt * L.nq * nt * 4);
   L.ndec = ndec;
-  L.off_rowp = o;   o = align16(o + ns * mt * L.kp * 8);
+  L.off_rowp = o;   o = align16(o + (ns * mt * L.kp + 8) * 8);
   L.off_info = o;   o = align16(o + ns * mt * 16);
   L.off_tR = o;     o = align16(o + ns * mt * L.r1 * 4);
   L.off_task = o;   o = align16(o + ns * mt * 4);

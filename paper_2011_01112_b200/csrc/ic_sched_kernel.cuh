@@ -83,8 +83,8 @@ __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax
 // general path with runtime kr options and per-option release masks).
 template <int NW, bool SB, bool DROP, int K, bool GEN>
 __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
-                                       const int4* __restrict__ ops4, const int d, const int r, const int kr,
-                                       const int pad) {
+                                       const int4* __restrict__ ops4, const int4 (&pre)[4], const int d,
+                                       const int r, const int kr, const int pad) {
   constexpr int NT = 32 * NW;
   constexpr int KK = GEN ? KMAX : K;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -92,7 +92,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 #pragma unroll
   for (int k = 0; k < KK; k += 2) {
     if (!GEN || k < kr) {
-      const int4 o = ops4[k >> 1];
+      const int4 o = k < 8 ? pre[k >> 1] : ops4[k >> 1];  // the first 8 were loaded before the dispatch
       C[k] = o.x;
       key[k] = o.y;
       if (k + 1 < KK) {
@@ -200,12 +200,13 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 template <int NW, bool SB, bool DROP>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
                                                 uint32_t* decrow, const int4* ops4, int d, int r, int pad) {
+  const int4 pre[4] = {ops4[0], ops4[1], ops4[2], ops4[3]};  // issued ahead of the K dispatch
   if (gen) {
-    dp_row<NW, SB, DROP, KMAX, true>(cur, nxt, decrow, ops4, d, r, K, pad);
+    dp_row<NW, SB, DROP, KMAX, true>(cur, nxt, decrow, ops4, pre, d, r, K, pad);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: dp_row<NW, SB, DROP, KK, false>(cur, nxt, decrow, ops4, d, r, K, pad); break;
+  case KK: dp_row<NW, SB, DROP, KK, false>(cur, nxt, decrow, ops4, pre, d, r, K, pad); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -681,7 +682,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       f = fn;
       ops += kp;
       decrow += dec_row_words;
-      bar_sync(BAR_DP, NT);
+      if (NW == 1)
+        __syncwarp();
+      else
+        bar_sync(BAR_DP, NT);
     }
     // a5: Q* = G_N(T), t* = least t with G_N(t) = Q*  (G_N non-decreasing on [0, d_N])
     if (warp == 0) {
