@@ -46,22 +46,25 @@ def _sms():
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
-def algorithmic_evals(inputs, n_tasks, opt_stride, chunk=65536):
+def algorithmic_evals(inputs, n_tasks, opt_stride, delta_micro=0, eps_micro=100_000, chunk=16384):
     """Algorithmic option evaluations of a batch (measurement only; torch ops on the inputs).
 
-    Returns (W_active, W_survey):
-      W_survey = sum_i [(T+1) + sum_k #{t <= d_i : t - C_i(k) >= r_i}], T = max(0, max_i d_i)
-                 (SURVEY.md §8(d): every row evaluates every column of the time axis);
-      W_active = sum_i [(d_i + 1)^+ + sum_k #{t <= d_i : t - C_i(k) >= r_i}]
-                 (this kernel: columns t > d_i of row i share one value, DESIGN.md §5,
-                 so only the active columns t <= d_i are evaluated).
-    Each evaluation reads one 4-byte DP cell from shared memory."""
+    Returns (W_active, W_survey).  W_survey = sum_i [(T+1) + sum_k #{t <= d_i : t - C_i(k) >= r_i}],
+    T = max(0, max_i d_i).  W_active counts what this kernel evaluates on the
+    axis it picks per instance: on the time axis
+      sum_i [(d_i + 1)^+ + sum_k #{t <= d_i : t - C_i(k) >= r_i}]
+    (columns past d_i share one value), on the reward axis (the paper's P(i, r), chosen when its
+    estimate sum_i (Qpre_i + 1)(K_i + 1) is the smaller, no releases)
+      sum_i [(Qpre_i + 1) + sum_{k < K_i} (Qpre_i - q_i(k) + 1)^+],
+    Qpre_i = prefix over EDF order of max_k q_i(k).  Each evaluation reads one 4-byte DP cell."""
     import torch
     B = inputs["task_begin"].numel() - 1
     wa = ws = 0
+    N = n_tasks
     for lo in range(0, B, chunk):
         hi = min(B, lo + chunk)
-        sl = slice(lo * n_tasks, hi * n_tasks)
+        nb = hi - lo
+        sl = slice(lo * N, hi * N)
         m = inputs["mand_wcet"][sl].long()
         ow = inputs["opt_wcet"][sl].long()
         S = inputs["n_opt"][sl].long()
@@ -71,10 +74,36 @@ def algorithmic_evals(inputs, n_tasks, opt_stride, chunk=65536):
         valid = k <= S[:, None]
         d = inputs["deadline"][sl].long()
         r = inputs["release"][sl].long()
-        opts = int((torch.clamp(d[:, None] - r[:, None] - C + 1, min=0) * valid).sum())
-        T = torch.clamp(d.view(-1, n_tasks).max(1).values, min=0)
-        ws += int(((T + 1) * n_tasks).sum()) + opts
-        wa += int(torch.clamp(d + 1, min=0).sum()) + opts
+        fit = (C <= (d - r)[:, None]) & valid
+        K = fit.sum(1)
+        opts = torch.clamp(d[:, None] - r[:, None] - C + 1, min=0) * valid
+        T = torch.clamp(d.view(nb, N).max(1).values, min=0)
+        ws += int(((T + 1) * N).sum() + opts.sum())
+        wt_inst = (torch.clamp(d + 1, min=0) + opts.sum(1)).view(nb, N).sum(1)
+        # reward axis (replicates the kernel's per-instance choice)
+        R = inputs["mand_conf"][sl].long()[:, None] + torch.cat(
+            [torch.zeros_like(m)[:, None], torch.cumsum(inputs["opt_gain"][sl].long(), 1)], 1)
+        if delta_micro:
+            dl = torch.full((nb,), delta_micro, dtype=torch.long, device=C.device)
+        else:
+            feas = ((r[:, None] + C) <= d[:, None]) & valid
+            rmax = torch.where(feas, R, torch.zeros_like(R)).max(1).values.view(nb, N).max(1).values
+            dl = torch.clamp(eps_micro * rmax // (1_000_000 * N), min=1)
+        q = torch.where(valid, R // dl.repeat_interleave(N)[:, None], torch.zeros_like(R))
+        qmax = q.max(1).values.view(nb, N)
+        key = d.view(nb, N) * (N + 1) + torch.arange(N, device=C.device)[None, :]  # EDF (d, idx); r = 0 here
+        order = torch.argsort(key, 1)
+        qpre = torch.cumsum(torch.gather(qmax, 1, order), 1)
+        Kg = torch.gather(K.view(nb, N), 1, order)
+        qg = torch.gather(q.view(nb, N, -1), 1, order[:, :, None].expand(-1, -1, q.shape[1]))
+        kk = torch.arange(q.shape[1], device=C.device)[None, None, :]
+        ropt = (torch.clamp(qpre[:, :, None] - qg + 1, min=0) * (kk < Kg[:, :, None])).sum(2)
+        wr_inst = ((qpre + 1) + ropt).sum(1)
+        est_t = (torch.clamp(d + 1, min=0).view(nb, N) * (K.view(nb, N) + 1)).sum(1)
+        est_r = ((qpre + 1) * (Kg + 1)).sum(1)
+        norel = (r.view(nb, N) == 0).all(1)
+        use_r = norel & (est_r < est_t)
+        wa += int(torch.where(use_r, wr_inst, wt_inst).sum())
     return wa, ws
 
 
@@ -249,7 +278,7 @@ def main():
     stream.synchronize()
     T = n_inst * cw.n_tasks
     in_bytes = sum(v.numel() * v.element_size() for v in inputs.values())
-    W, W_survey = algorithmic_evals(inputs, cw.n_tasks, cw.n_opt)
+    W, W_survey = algorithmic_evals(inputs, cw.n_tasks, cw.n_opt, args.delta_micro, cw.epsilon_micro)
 
     sc = pkg.SchedConfig(device=local, max_tasks=cw.n_tasks, max_opt_stages=cw.n_opt, max_horizon=cw.horizon,
                          delta_micro=args.delta_micro, epsilon_micro=cw.epsilon_micro)

@@ -35,8 +35,8 @@ inline int align16(int x) { return (x + 15) & ~15; }
 struct Layout {
   int bytes, nq, kp, r1, np2, pad, rs, nbuf;
   int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
-      off_sS, off_key;
-  int nslots, ndec;
+      off_sS, off_key, off_aux, off_sQ;
+  int nslots, ndec, cap;
 };
 
 Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_smem, int nslots = 2,
@@ -66,12 +66,15 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
   L.off_tR = o;     o = align16(o + ns * mt * L.r1 * 4);
   L.off_task = o;   o = align16(o + ns * mt * 4);
   L.off_tail = o;   o = align16(o + ns * mt * 4);
-  L.off_misc = o;   o = align16(o + 2 * 16 * 8);
+  L.off_misc = o;   o = align16(o + 3 * 16 * 8);
   L.off_chosen = o; o = align16(o + mt * 4);
   L.off_sd = o;     o = align16(o + mt * 4);
   L.off_sr = o;     o = align16(o + mt * 4);
   L.off_sS = o;     o = align16(o + mt * 4);
   L.off_key = o;    o = align16(o + L.np2 * 8);
+  L.off_aux = o;    o = align16(o + ns * mt * 4);
+  L.off_sQ = o;     o = align16(o + mt * 4);
+  L.cap = cap;
   L.bytes = o;
   return L;
 }
@@ -288,6 +291,10 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   p.off_key = L.off_key;
   p.rowbuf_stride = L.rs;
   p.nslots = L.nslots;
+  p.cap = L.cap;
+  p.off_aux = L.off_aux;
+  p.off_sQ = L.off_sQ;
+  p.axis_mode = env_int("IC_SCHED_AXIS", 0);
   p.work = h->work;
   p.ndec = L.ndec;
   p.dec_words = (int64_t)h->cfg.max_tasks * L.nq * 32 * h->nw;

@@ -35,6 +35,7 @@
 namespace icsched {
 
 constexpr int NEG = -(1 << 30);
+constexpr int INFV = 1 << 30;  // reward axis: unreachable (packed finish time)
 constexpr int KMAX = 15;           // options per task: mandatory-only .. 14 optional stages
 constexpr int BAR_DP = 1, BAR_READY = 2, BAR_DONE = 3;
 constexpr int ST_OK = 0, ST_INFEASIBLE = 1, ST_BAD = 2, ST_LIMIT = 3, ST_END = -1;
@@ -66,6 +67,9 @@ struct Params {
   int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
       off_sS, off_key;
   int nslots;  // 2: set up instance b+1 while the DP sweeps b; 1: serialised (large N)
+  int cap;     // row buffer capacity in columns (32 NW x COLS)
+  int off_aux, off_sQ;
+  int axis_mode;  // 0 auto (per instance), 1 time axis only, 2 reward axis whenever eligible
   unsigned long long* work;  // [2] dynamic instance counter, CTAs finished (reset by the last CTA)
   int rowbuf_stride;  // ints per row buffer (pad + capacity)
 };
@@ -81,10 +85,15 @@ __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax
 // ---------------------------------------------------------------------------
 // DP warps: one row, active columns t <= d.  K options (compile-time; GEN =
 // general path with runtime kr options and per-option release masks).
-template <int NW, bool SB, bool DROP, int K, bool GEN>
+// RW = the reward-indexed axis (NEXT-1, the paper's own Eqs. 1-2): a cell holds the
+// least finish time P(i, r)*16 of the first i EDF tasks reaching exactly quantised
+// reward r; option k shifts by q_k and adds C_k*16 + (k+1) (the code), so one
+// VIADDMNMX (add + min) per option yields value and argmin, ties to the smaller
+// code (drop, then fewer stages).  Admits are valid iff P <= d_i ("lim").
+template <int NW, bool SB, bool DROP, int K, bool GEN, bool RW>
 __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
                                        const int4* __restrict__ ops4, const int4 (&pre)[4], const int d,
-                                       const int r, const int kr, const int pad) {
+                                       const int r, const int kr, const int pad, const int lim) {
   constexpr int NT = 32 * NW;
   constexpr int KK = GEN ? KMAX : K;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -101,29 +110,51 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       }
     }
   }
+  int reachC = 0;
+  if (RW) {  // (C, (q<<4)-(k+1)) -> shift q, add C*16 + k+1
+#pragma unroll
+    for (int k = 0; k < KK; ++k) {
+      const int q = (key[k] + k + 1) >> 4;
+      key[k] = min(C[k], 1 << 20) * 16 + (k + 1);
+      C[k] = q;
+      reachC = max(reachC, q);
+    }
+  } else if (KK > 0) {
+    reachC = C[KK - 1];
+  }
   const int w0 = warp * 32;
   const int ng = d >= w0 ? (d - w0) / NT + 1 : 0;  // this warp's groups holding a column t <= d
-  // groups whose longest option reaches left of the NEG pad read through a clamp
-  const int reach = (!GEN && KK > 0) ? C[KK > 0 ? KK - 1 : 0] - pad - w0 : 0;
+  // groups whose longest option reaches left of the pad read through a clamp
+  const int reach = (!GEN && KK > 0) ? reachC - pad - w0 : 0;
   const int gcl = GEN ? ng : (reach > 0 ? (reach + NT - 1) / NT : 0);
   auto cell = [&](int t, auto clamp_tag) -> int {
     constexpr bool CL = decltype(clamp_tag)::value;
-    int v = DROP ? cur[t] : NEG;
+    if constexpr (RW) {
+      int a = INFV;
 #pragma unroll
-    for (int k = 0; k < KK; ++k) {
-      if (GEN) {  // releases: options with a source before r are invalid (read a NEG cell)
-        if (k < kr) {
-          const int src = t - C[k];
-          v = viaddmax(cur[src >= r ? src : -1], key[k], v);
+      for (int k = 0; k < KK; ++k) a = __viaddmin_s32(cur[CL ? max(t - C[k], -pad) : t - C[k]], key[k], a);
+      a = a <= lim ? a : INFV;
+      return DROP ? min(cur[t], a) : a;
+    } else {
+      int v = DROP ? cur[t] : NEG;
+#pragma unroll
+      for (int k = 0; k < KK; ++k) {
+        if (GEN) {  // releases: options with a source before r are invalid (read a NEG cell)
+          if (k < kr) {
+            const int src = t - C[k];
+            v = viaddmax(cur[src >= r ? src : -1], key[k], v);
+          }
+        } else if (CL) {
+          v = viaddmax(cur[max(t - C[k], -pad)], key[k], v);
+        } else {
+          v = viaddmax(cur[t - C[k]], key[k], v);
         }
-      } else if (CL) {
-        v = viaddmax(cur[max(t - C[k], -pad)], key[k], v);
-      } else {
-        v = viaddmax(cur[t - C[k]], key[k], v);
       }
+      return v;
     }
-    return v;
   };
+  // stored value: time axis keeps low nibble 15 (the drop key), reward axis keeps it 0
+  auto stv = [](int v) { return RW ? (v & ~15) : (v | 15); };
   if (!SB) {
     constexpr int BATCH = (KK <= 6) ? 8 : 4;  // cells whose loads are in flight together
     auto chunk = [&](int g0, auto clamp_tag) {
@@ -138,7 +169,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 #pragma unroll
           for (int u = 0; u < BATCH; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
-            nxt[tb + (h + u) * NT] = v[u] | 15;
+            nxt[tb + (h + u) * NT] = stv(v[u]);
           }
         }
       } else {
@@ -153,7 +184,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (u0 + u));
-            nxt[tb + (u0 + u) * NT] = v[u] | 15;
+            nxt[tb + (u0 + u) * NT] = stv(v[u]);
           }
           u0 += NB;
         };
@@ -189,7 +220,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       for (int u = 0; u < 8; ++u) {
         if (g0 + u < ng) {
           dw |= (uint32_t)(v[u] & 15) << (4 * u);
-          nxt[tb + u * NT] = v[u] | 15;
+          nxt[tb + u * NT] = stv(v[u]);
         }
       }
       if (g0 < ng) decrow[(g0 >> 3) * NT + tid] = dw;
@@ -197,16 +228,17 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   }
 }
 
-template <int NW, bool SB, bool DROP>
+template <int NW, bool SB, bool DROP, bool RW>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
-                                                uint32_t* decrow, const int4* ops4, int d, int r, int pad) {
+                                                uint32_t* decrow, const int4* ops4, int d, int r, int pad,
+                                                int lim) {
   const int4 pre[4] = {ops4[0], ops4[1], ops4[2], ops4[3]};  // issued ahead of the K dispatch
-  if (gen) {
-    dp_row<NW, SB, DROP, KMAX, true>(cur, nxt, decrow, ops4, pre, d, r, K, pad);
+  if (!RW && gen) {
+    dp_row<NW, SB, DROP, KMAX, true, false>(cur, nxt, decrow, ops4, pre, d, r, K, pad, lim);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: dp_row<NW, SB, DROP, KK, false>(cur, nxt, decrow, ops4, pre, d, r, K, pad); break;
+  case KK: dp_row<NW, SB, DROP, KK, false, RW>(cur, nxt, decrow, ops4, pre, d, r, K, pad, lim); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -248,6 +280,8 @@ struct Smem {
   long long* misc;  // [2][16]
   int32_t* chosen;  // [max_tasks]
   int32_t *sd, *sr, *sS;  // staging (input order), tail warp only
+  int32_t* aux;  // [2][max_tasks]  reward axis: admit limit d_i*16+15 of EDF row pos
+  int32_t* sQ;   // [max_tasks]     staging: prefix of max quantised reward
   unsigned long long* key;
 };
 
@@ -373,42 +407,77 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     }
   }
   __syncwarp();
-  // pass 2: the row table in EDF order
-  long long qsum = 0;
-  for (int pos = lane; pos < n; pos += 32) {
-    const int tk = (int)(S.key[pos] & 0xFFF);
-    const int64_t t = lo + tk;
-    const int d = S.sd[tk], r = S.sr[tk], Sn = S.sS[tk];
-    int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
-    int32_t* trp = S.tR + ((size_t)s * p.max_tasks + pos) * p.r1;
-    long long C = p.mand_wcet[t], R = p.mand_conf[t];
-    int K = 0, qmax = 0;
-    auto option = [&](int k) {
-      const int q = (int)(R / delta);
-      qmax = max(qmax, q);
-      if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
-        rp[k] = make_int2((int)C, (q << 4) - (k + 1));
-        trp[k] = (int)R;
-        K = k + 1;
-      }
-    };
-    option(0);
-    for_each_opt(p, t, Sn, [&](int k, int w, int g) {
-      C += w;
-      R += g;
-      option(k);
-    });
+  // pass 2: the row table in EDF order (32 rows at a time, prefix of max q by warp scan)
+  long long qsum = 0, wt = 0, wr = 0;
+  int anyrel = 0, qcarry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int pos = base + lane;
+    int qmax = 0, K = 0, d = 0;
+    if (pos < n) {
+      const int tk = (int)(S.key[pos] & 0xFFF);
+      const int64_t t = lo + tk;
+      d = S.sd[tk];
+      const int r = S.sr[tk], Sn = S.sS[tk];
+      int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
+      int32_t* trp = S.tR + ((size_t)s * p.max_tasks + pos) * p.r1;
+      long long C = p.mand_wcet[t], R = p.mand_conf[t];
+      auto option = [&](int k) {
+        const int q = (int)(R / delta);
+        qmax = max(qmax, q);
+        if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
+          rp[k] = make_int2((int)C, (q << 4) - (k + 1));
+          trp[k] = (int)R;
+          K = k + 1;
+        }
+      };
+      option(0);
+      for_each_opt(p, t, Sn, [&](int k, int w, int g) {
+        C += w;
+        R += g;
+        option(k);
+      });
+      const bool gen = r > 0;  // releases take the masked path; long options clamp per group
+      anyrel |= r > 0;
+      const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
+      S.info[s * p.max_tasks + pos] = make_int4(d, K | (gen ? 256 : 0) | (Sn << 16), r, dn);
+      S.task[s * p.max_tasks + pos] = tk;
+      S.aux[s * p.max_tasks + pos] = d * 16 + 15;
+    }
     qsum += qmax;
-    const bool gen = r > 0;  // releases take the masked path; long options clamp per group
-    const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
-    S.info[s * p.max_tasks + pos] = make_int4(d, K | (gen ? 256 : 0) | (Sn << 16), r, dn);
-    S.task[s * p.max_tasks + pos] = tk;
+    int inc = qmax;  // inclusive scan: Qpre(pos) = sum of max q over EDF rows <= pos
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int qpre = qcarry + inc;
+    if (pos < n) {
+      S.sQ[pos] = qpre;
+      wt += (long long)max(d + 1, 0) * (K + 1);  // active cells x options, both axes
+      wr += (long long)(qpre + 1) * (K + 1);
+    }
+    qcarry = __shfl_sync(0xffffffffu, qpre, 31);
   }
   qsum = warp_sum64(qsum);
+  wt = warp_sum64(wt);
+  wr = warp_sum64(wr);
+  anyrel = __any_sync(0xffffffffu, anyrel);
   if (qsum * 16 + 16LL * n >= (1LL << 30)) {
     write_dropped(p, b, lo, n, ST_LIMIT, lane);
     if (lane == 0) { acc[0] += 1; acc[3] += 1; }
     return ST_LIMIT;
+  }
+  __syncwarp();
+  // a4 axis: the paper's reward-indexed table (Eqs. 1-2) when it is the smaller sweep
+  // (e.g. Delta = 0.1), else its time-indexed dual.  Releases need the
+  // budget-tracked backtrack, so they stay on the time axis.
+  const bool rw = p.axis_mode != 1 && !anyrel && qcarry + 1 <= p.cap && (p.axis_mode == 2 || wr < wt);
+  if (rw) {
+    for (int pos = lane; pos < n; pos += 32) {
+      int4* f = S.info + s * p.max_tasks + pos;
+      f->x = S.sQ[pos];
+      f->w = pos + 1 < n ? S.sQ[pos + 1] : INT32_MIN;
+    }
   }
   __syncwarp();
   if (lane == 0) {
@@ -420,6 +489,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     mi[4] = delta;
     mi[7] = S.info[s * p.max_tasks].x;
     mi[8] = S.info[s * p.max_tasks + n - 1].x;
+    mi[9] = rw ? 1 : 0;
   }
   __syncwarp();
   return ST_OK;
@@ -436,19 +506,25 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
       int t = (int)mi[6];
       const int4* inf = S.info + s * p.max_tasks;
       const int2* rp = S.rowp + (size_t)s * p.max_tasks * p.kp;
+      const bool rw = mi[9] != 0;
       for (int pos = n - 1; pos >= 0; --pos) {
-        const int d = inf[pos].x;
+        const int d = inf[pos].x;  // time axis: deadline; reward axis: last reachable column
         int nib;
-        if (t > d) {
+        if (!rw && t > d) {
           nib = S.tail[s * p.max_tasks + pos];
         } else {
           const int g = t / NT, l = t - g * NT;
           const uint32_t w = S.dec[db * p.dec_words + ((size_t)pos * p.nq + (g >> 3)) * NT + l];
           nib = (int)((w >> (4 * (g & 7))) & 15u);
         }
-        const int code = 15 - nib;
-        S.chosen[pos] = code;
-        if (code > 0) t = min(t, d) - rp[(size_t)pos * p.kp + code - 1].x;
+        if (rw) {  // reward axis: the nibble is the code; step to column r - q
+          S.chosen[pos] = nib;
+          if (nib > 0) t -= (rp[(size_t)pos * p.kp + nib - 1].y + nib) >> 4;
+        } else {
+          const int code = 15 - nib;
+          S.chosen[pos] = code;
+          if (code > 0) t = min(t, d) - rp[(size_t)pos * p.kp + code - 1].x;
+        }
       }
     }
   }
@@ -560,6 +636,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
   S.sr = (int32_t*)(smem + p.off_sr);
   S.sS = (int32_t*)(smem + p.off_sS);
   S.key = (unsigned long long*)(smem + p.off_key);
+  S.aux = (int32_t*)(smem + p.off_aux);
+  S.sQ = (int32_t*)(smem + p.off_sQ);
   const int RS = p.rowbuf_stride;
   for (int bb = 0; bb < (SB ? 1 : 2); ++bb)
     for (int i = tid; i < p.pad; i += blockDim.x) S.rowbuf[bb * RS + i] = NEG;
@@ -631,6 +709,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
   // ================= DP warps =================
   const int RSb = SB ? 0 : RS;
   int32_t* buf0 = S.rowbuf + p.pad;
+  int padmode = 0;  // value in the pad cells: 0 NEG (time axis), 1 INFV (reward axis)
+  int* rmax_slot = (int*)(S.misc + 2 * 16);  // reward axis: CTA max over finite columns
   for (int it = 0;; ++it) {
     bar_sync(BAR_READY, NT + 32);
     const int s = p.nslots == 2 ? (it & 1) : 0;
@@ -639,10 +719,22 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     if (mi[3] == ST_END) break;
     const int n = (int)mi[0];
     const int d_first = (int)mi[7];
-    for (int t = tid; t <= d_first; t += NT) buf0[t] = 15;  // G_0(t) = 0
+    const bool rw = mi[9] != 0;
+    if ((int)rw != padmode) {  // the pad left of column 0 must read as "invalid" for this axis
+      padmode = rw;
+      for (int bb = 0; bb < (SB ? 1 : 2); ++bb)
+        for (int i = tid; i < p.pad; i += NT) S.rowbuf[bb * RS + i] = rw ? INFV : NEG;
+    }
+    if (rw) {  // P(0, 0) = 0, P(0, r > 0) = infinity
+      for (int t = tid; t <= d_first; t += NT) buf0[t] = t == 0 ? 0 : INFV;
+      if (tid == 0) *rmax_slot = -1;
+    } else {
+      for (int t = tid; t <= d_first; t += NT) buf0[t] = 15;  // G_0(t) = 0
+    }
     bar_sync(BAR_DP, NT);
     const int4* inf = S.info + s * p.max_tasks;
     const int2* rpb = S.rowp + (size_t)s * p.max_tasks * p.kp;
+    const int32_t* auxp = S.aux + s * p.max_tasks;
     int M = 15;
     int4 f = inf[0];
     int32_t* const tailp = S.tail + s * p.max_tasks;
@@ -657,28 +749,39 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       const bool gen = (f.y >> 8) & 1;
       const int32_t* cur = buf0 + (pos & 1) * RSb;
       int32_t* nxt = buf0 + ((pos + 1) & 1) * RSb;
-      // admit value at column d: every column t > d shares it (tail collapse).  In
-      // double-buffered mode its loads are issued here and consumed after the sweep.
-      int av = NEG;
-      if (lane < K) {
-        const int2 o = ops[lane];
-        const int src = d - o.x;
-        if (src >= r) av = cur[src] + o.y;
-      }
-      int A = 0;
-      if (SB) A = __reduce_max_sync(0xffffffffu, av);
-      dp_row_dispatch<NW, SB, DROP>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, p.pad);
-      if (!SB) A = __reduce_max_sync(0xffffffffu, av);
-      const int Mv = DROP ? max(M, A) : A;
-      if (tid == 0) tailp[pos] = Mv & 15;
-      const int Mn = Mv | 15;
-      // G_pos(t) = M_pos on (d, d_next]: the next row reads it there
-      if (dn > d) {
-        const int first = d + 1 > 0 ? d + 1 : 0;
+      if (rw) {
+        // reward axis: columns r <= Qpre_pos; (Qpre_pos, Qpre_next] are unreachable
+        dp_row_dispatch<NW, SB, DROP, true>(K, false, cur, nxt, decrow, (const int4*)ops, d, 0, p.pad,
+                                            auxp[pos]);
+        if (dn > d) {
+          const int first = d + 1;
 #pragma unroll 1
-        for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = Mn;
+          for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = INFV;
+        }
+      } else {
+        // admit value at column d: every column t > d shares it (tail collapse).  In
+        // double-buffered mode its loads are issued here and consumed after the sweep.
+        int av = NEG;
+        if (lane < K) {
+          const int2 o = ops[lane];
+          const int src = d - o.x;
+          if (src >= r) av = cur[src] + o.y;
+        }
+        int A = 0;
+        if (SB) A = __reduce_max_sync(0xffffffffu, av);
+        dp_row_dispatch<NW, SB, DROP, false>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, p.pad, 0);
+        if (!SB) A = __reduce_max_sync(0xffffffffu, av);
+        const int Mv = DROP ? max(M, A) : A;
+        if (tid == 0) tailp[pos] = Mv & 15;
+        const int Mn = Mv | 15;
+        // G_pos(t) = M_pos on (d, d_next]: the next row reads it there
+        if (dn > d) {
+          const int first = d + 1 > 0 ? d + 1 : 0;
+#pragma unroll 1
+          for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = Mn;
+        }
+        M = Mn;
       }
-      M = Mn;
       f = fn;
       ops += kp;
       decrow += dec_row_words;
@@ -687,10 +790,22 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       else
         bar_sync(BAR_DP, NT);
     }
-    // a5: Q* = G_N(T), t* = least t with G_N(t) = Q*  (G_N non-decreasing on [0, d_N])
-    if (warp == 0) {
-      const int dl = (int)mi[8];
-      const int32_t* fin = buf0 + (n & 1) * RSb;
+    const int32_t* fin = buf0 + (n & 1) * RSb;
+    const int dl = (int)mi[8];
+    if (rw) {
+      // a5 (reward axis): r* = the largest finite column of row N (reading R6)
+      int best = -1;
+      for (int t = tid; t <= dl; t += NT)
+        if (fin[t] < INFV) best = t;
+      best = __reduce_max_sync(0xffffffffu, best);
+      if (lane == 0) atomicMax(rmax_slot, best);
+      bar_sync(BAR_DP, NT);
+      if (tid == 0) {
+        mi[5] = *rmax_slot;
+        mi[6] = *rmax_slot;
+      }
+    } else if (warp == 0) {
+      // a5: Q* = G_N(T), t* = least t with G_N(t) = Q*  (G_N non-decreasing on [0, d_N])
       long long Qv, ts = 0;
       if (dl < 0) {
         Qv = M;

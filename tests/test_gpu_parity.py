@@ -248,3 +248,36 @@ def test_c5_sweep_blocks():
     tb = batch.task_begin
     drops = [(got["kept"][tb[b]:tb[b + 1]] < 0).mean() for b in range(batch.n_instances)]
     assert np.mean(drops[-12:]) > np.mean(drops[:12])
+
+
+@pytest.mark.parametrize("axis", ["1", "2"])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("delta", [100_000, 20_000, 0])
+def test_reward_axis(monkeypatch, axis, mode, delta):
+    """NEXT-1: the reward-indexed sweep (the paper's P(i, r) table, forced with IC_SCHED_AXIS=2)
+    and the time axis (IC_SCHED_AXIS=1) give the same canonical plans; instances with releases
+    stay on the time axis."""
+    monkeypatch.setenv("IC_SCHED_AXIS", axis)
+    rng = np.random.default_rng(31 + mode + delta)
+    parts = [gen.tiny_random(rng, 6000, max_tasks=6, max_opt=3, horizon=40, p_release=0.0),
+             gen.tiny_random(rng, 500, max_tasks=6, max_opt=3, horizon=40, p_release=0.5)]
+    batch = gen.concat(parts, 3)
+    ocfg = OracleConfig(drop_mode=mode, delta_micro=delta, epsilon_micro=300_000, max_tasks=6, max_horizon=40)
+    ref = oracle.solve(batch, ocfg, BRUTE)
+    got = gpu_solve(batch, max_tasks=6, max_opt=3, max_horizon=40, drop_mode=mode, delta=delta, eps=300_000)
+    assert_parity(got, ref, f"axis={axis} mode={mode} delta={delta}")
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_reward_axis_paper_delta(monkeypatch, name, mode):
+    """At the paper's Delta = 0.1 the reward axis is the shorter sweep and is auto-selected."""
+    cw = gen.CONFIGS[name]
+    batch = gen.generate(cw, {"C2": 300, "C3": 60, "C4": 2}[name])
+    ocfg = OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=cw.n_tasks, max_horizon=cw.horizon)
+    ref = oracle.solve(batch, ocfg, TIME)
+    for axis in ("0", "1", "2"):
+        monkeypatch.setenv("IC_SCHED_AXIS", axis)
+        got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
+                        delta=100_000)
+        assert_parity(got, ref, f"{name} axis={axis} mode={mode}")
