@@ -6,10 +6,14 @@
 
 One step = one pass of the whole hot path (descriptor
 load, prefix/quantise, EDF sort, DP sweep, backtrack, schedule, stats) over
-one batch of the configuration's instances, inputs resident in HBM (each rank
-generates its own global-id shard on device; weak scaling: every rank solves
-a full batch), followed by the NCCL all-reduce of the int64 stats vector when
-N > 1.  Rank 0 prints one JSON line.
+one batch of the configuration's instances, inputs resident in HBM, followed by
+the NCCL all-reduce of the int64 stats vector when N > 1.  The default workload
+is C5, the configuration BASELINE.json's metric ("instances solved/sec at
+1/2/4/8 B200") is quoted on: 2^24 instances of the C3 shape in four
+utilisation blocks U = 1, 2, 4, 8, split over the ranks (strong scaling; each
+rank generates its own contiguous global-id shard on device).  C1-C4 are
+weak-scaled (every rank solves a full batch of distinct ids).  Rank 0 prints
+one JSON line.
 """
 from __future__ import annotations
 
@@ -160,12 +164,24 @@ def workload_config(cw, args, n_instances):
             "horizon": cw.horizon, "seed": hex(cw.seed)}
 
 
+def sample_batch(cw, n, salt=0):
+    """n instances of the workload for the CPU oracle; C5 draws equally from its U blocks."""
+    if not cw.u_blocks:
+        return gen.generate(cw, n, id_offset=salt)
+    parts, start = [], 0
+    per = max(1, n // len(cw.u_blocks))
+    for _, cnt in cw.u_blocks:
+        parts.append(gen.generate(cw, per, id_offset=start + salt))
+        start += cnt
+    return gen.concat(parts, cw.n_opt)
+
+
 def _calibrate_oracle(cw, ocfg, threads, target_s):
     """Instances of `cw` the oracle solves in about target_s seconds on `threads` threads."""
     import oracle
     n = max(threads * 4, 32)
     while True:
-        sample = gen.generate(cw, n, id_offset=1 << 30)
+        sample = sample_batch(cw, n, salt=1 << 20)
         t0 = time.perf_counter()
         oracle.solve(sample, ocfg, oracle.PAPER, threads)
         dt = time.perf_counter() - t0
@@ -181,7 +197,8 @@ def cpu_oracle_rate(cw, args, target_s):
     ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
                                max_tasks=cw.n_tasks, max_horizon=cw.horizon)
     n = _calibrate_oracle(cw, ocfg, threads, target_s)
-    sample = gen.generate(cw, n)
+    sample = sample_batch(cw, n)
+    n = sample.n_instances
     t0 = time.perf_counter()
     oracle.solve(sample, ocfg, oracle.PAPER, threads)
     el = time.perf_counter() - t0
@@ -196,9 +213,11 @@ def run_reference(args, cw, rank, world):
     threads = os.cpu_count() or 1
     ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
                                max_tasks=cw.n_tasks, max_horizon=cw.horizon)
-    # size each step for ~10 s of CPU work so K+W steps stay within a few minutes
-    n = _calibrate_oracle(cw, ocfg, threads, 10.0)
-    sample = gen.generate(cw, n)
+    # size each step so the whole K+W-step run stays near two minutes of CPU work
+    per_step = min(10.0, max(1.0, 120.0 / (args.steps + args.warmup)))
+    n = _calibrate_oracle(cw, ocfg, threads, per_step)
+    sample = sample_batch(cw, n)
+    n = sample.n_instances
     for _ in range(args.warmup):
         oracle.solve(sample, ocfg, oracle.PAPER, threads)
     t0 = time.perf_counter()
@@ -221,7 +240,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="timed steps (default: >= 1 s of work)")
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5", help="C5 (default): the 2^24-instance overload sweep the metric is quoted on at 1/2/4/8 GPUs; C1-C4 are the other BASELINE.json configs")
     ap.add_argument("--instances", type=int, default=0, help="override instances per GPU")
     ap.add_argument("--delta-micro", type=int, default=0, help="fixed Delta instead of FPTAS eps")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -254,26 +273,41 @@ def main():
     if strong:
         id0, id1 = shard_range(cw.n_instances, rank, world)
         n_inst = id1 - id0
+        spans = []  # (global id lo, hi) pieces of this rank's shard
+        start = 0
+        for _, cnt in cw.u_blocks:
+            lo, hi = max(id0, start), min(id1, start + cnt)
+            spans.append((lo, hi) if lo < hi else None)
+            start += cnt
+    elif cw.u_blocks:  # --instances with C5: an equal slice from the start of every U block (profiling)
+        per = args.instances // len(cw.u_blocks)
+        n_inst = per * len(cw.u_blocks)
+        spans, start = [], 0
+        for _, cnt in cw.u_blocks:
+            spans.append((start + rank * per, start + (rank + 1) * per))
+            start += cnt
     else:
         n_inst = args.instances or cw.n_instances
         id0 = weak_shard(n_inst, rank)[0]
+        spans = [(id0, id0 + n_inst)]
     stream = torch.cuda.Stream(dev)
 
     # ---- inputs resident in HBM: this rank's global-id shard, generated on device
     with torch.cuda.stream(stream):
         N = cw.n_tasks
         inputs = pkg.alloc_inputs(n_inst, n_inst * N, cw.n_opt, dev)
-        blocks = cw.u_blocks or ((None, cw.n_instances if strong else 1 << 62),)
-        start = 0 if cw.u_blocks else id0
-        for u, cnt in blocks:
-            lo, hi = max(id0, start), min(id0 + n_inst, start + cnt)
-            if lo < hi:
-                g = cw.gen_config(None, u, u) if u is not None else cw.gen_config()
-                a, z = lo - id0, hi - id0
-                view = {k: (v[a:z + 1] if k == "task_begin" else v[a * N:z * N]) for k, v in inputs.items()}
-                pkg.gen_batch_device(g.seed, g.n_tasks, g.n_opt, g.opt_stride, g.horizon, g.u_lo_q16,
-                                     g.u_hi_q16, g.d_lo, hi - lo, lo, device=dev, stream=stream, out=view)
-            start += cnt
+        a = 0
+        for bi, span in enumerate(spans):
+            if span is None:
+                continue
+            lo, hi = span
+            u = cw.u_blocks[bi][0] if cw.u_blocks else None
+            g = cw.gen_config(None, u, u) if u is not None else cw.gen_config()
+            z = a + hi - lo
+            view = {k: (v[a:z + 1] if k == "task_begin" else v[a * N:z * N]) for k, v in inputs.items()}
+            pkg.gen_batch_device(g.seed, g.n_tasks, g.n_opt, g.opt_stride, g.horizon, g.u_lo_q16,
+                                 g.u_hi_q16, g.d_lo, hi - lo, lo, device=dev, stream=stream, out=view)
+            a = z
         inputs["task_begin"].copy_(torch.arange(n_inst + 1, device=dev, dtype=torch.int64) * N)
     stream.synchronize()
     T = n_inst * cw.n_tasks
@@ -303,7 +337,7 @@ def main():
             step()
         e1.record(stream)
         e1.synchronize()
-        k = max(10, int(1000.0 / max(e0.elapsed_time(e1), 1e-3)) + 1)
+        k = max(3, int(1000.0 / max(e0.elapsed_time(e1), 1e-3)) + 1)
         kt = torch.tensor([k], device=dev)
         if world > 1:
             dist.all_reduce(kt, op=dist.ReduceOp.MAX)
@@ -341,12 +375,12 @@ def main():
         for k in hin:
             hin[k].copy_(inputs[k])
         hout = pkg.alloc_outputs(n_inst, T, host=True, pinned=True)
-        for _ in range(2):
+        for _ in range(1):
             sched.solve_batch_host(hin, hout, stream)
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ke = max(2, min(args.steps, 10))
+        ke = max(2, min(args.steps, 5))
         e0.record(stream)
         for _ in range(ke):
             sched.solve_batch_host(hin, hout, stream)
@@ -399,8 +433,9 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             v, n, el, thr = cpu_oracle_rate(cw, args, args.cpu_seconds)
             line["cpu_baseline"] = {"value": v, "unit": "instances/s", "cores": thr, "kind": "oracle",
-                                    "sample": f"{n} {cw.name} instances (ids 0..{n - 1}), paper "
-                                              f"reward-indexed DP (O2) on {thr} OpenMP threads, {el:.1f} s"}
+                                    "sample": f"{n} {cw.name} instances (" +
+                                              ("equal parts of every U block" if cw.u_blocks else f"ids 0..{n - 1}") +
+                                              f"), paper reward-indexed DP (O2) on {thr} OpenMP threads, {el:.1f} s"}
         print(json.dumps(line), flush=True)
     sched.close()
     if world > 1:

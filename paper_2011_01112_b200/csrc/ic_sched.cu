@@ -94,7 +94,9 @@ struct ic_sched {
   void* stage;
   size_t stage_bytes;
   cudaStream_t s_in, s_comp, s_out;  // host entry point: copy-in / compute / copy-out pipeline
-  cudaEvent_t ev[3 * 16 + 1];
+  cudaEvent_t ev[3 * 4 + 2];
+  int64_t* tb_pinned;  // [3][chunk+1] rebased CSR offsets of the staged chunks
+  int64_t tb_cap;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -204,6 +206,7 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
     cudaStreamDestroy(h->s_out);
     for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   }
+  if (h->tb_pinned) cudaFreeHost(h->tb_pinned);
   free(h);
   return IC_OK;
 }
@@ -306,10 +309,12 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
 }
 
 // Host-buffer entry point: H2D of the inputs, solve, D2H of the outputs.  The batch
-// is cut into up to 16 instance chunks pipelined over three internal streams
-// (copy-in, compute, copy-out) so PCIe traffic overlaps the sweep; kernels stay
-// serialised on the compute stream (they share the decision workspace).  Ordered
-// after prior work on `cuda_stream`; synchronised before returning.
+// is cut into instance chunks (>= 8, each <= ~256 MB staged) that cycle through a
+// ring of three device staging slots over three internal streams (copy-in,
+// compute, copy-out), so PCIe traffic overlaps the sweep and device memory stays
+// bounded whatever the batch size.  Kernels stay serialised on the compute stream
+// (they share the decision workspace).  Ordered after prior work on
+// `cuda_stream`; synchronised before returning.
 extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_batch_out* out,
                                          void* cuda_stream) {
   if (!h) return IC_ERR_INVALID_ARG;
@@ -327,70 +332,99 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
   }
   const int64_t B = in->n_instances;
   const int64_t* tbh = in->task_begin;
-  if (tbh[B] < tbh[0]) return IC_ERR_INVALID_ARG;
-  const int64_t T = tbh[B];  // task rows [0, T) are addressed by the CSR offsets
+  for (int64_t b = 0; b < B; ++b)
+    if (tbh[b + 1] < tbh[b]) return IC_ERR_INVALID_ARG;
   const int64_t st = h->cfg.max_opt_stages;
+  const int64_t T = tbh[B] - tbh[0];
+  const int64_t task_bytes = 4 * 5 + 1 + 8 * st + 9, inst_bytes = 8 * 4 + 4 + 1 + 8;
+  // chunk: at least 8 per batch for overlap, at most ~256 MB of staging
+  int64_t chunk = (B + 7) / 8;
+  const int64_t per_inst = (T / B + 1) * task_bytes + inst_bytes;
+  const int64_t lim = (256ll << 20) / per_inst;
+  if (chunk > lim) chunk = lim > 64 ? lim : 64;
+  if (chunk < 1) chunk = 1;
+  // the largest chunk's task count bounds the slot size
+  int64_t maxt = 0;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t b1 = b0 + chunk < B ? b0 + chunk : B;
+    if (tbh[b1] - tbh[b0] > maxt) maxt = tbh[b1] - tbh[b0];
+  }
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~(size_t)255; return o; };
-  const size_t o_tb = take((B + 1) * 8), o_r = take(T * 4), o_d = take(T * 4), o_m = take(T * 4),
-               o_n = take(T), o_ow = take(T * st * 4), o_mc = take(T * 4), o_og = take(T * st * 4),
-               o_k = take(T), o_s = take(T * 4), o_f = take(T * 4), o_q = take(B * 8), o_c = take(B * 8),
-               o_ct = take(B * 8), o_ms = take(B * 4), o_st = take(B), o_stats = take(64);
-  if (off > h->stage_bytes) {
+  const size_t o_tb = take((chunk + 1) * 8), o_r = take(maxt * 4), o_d = take(maxt * 4),
+               o_m = take(maxt * 4), o_n = take(maxt), o_ow = take(maxt * st * 4), o_mc = take(maxt * 4),
+               o_og = take(maxt * st * 4), o_k = take(maxt), o_s = take(maxt * 4), o_f = take(maxt * 4),
+               o_q = take(chunk * 8), o_c = take(chunk * 8), o_ct = take(chunk * 8), o_ms = take(chunk * 4),
+               o_st = take(chunk);
+  const size_t slot = off;
+  const size_t o_stats = 3 * slot;
+  if (o_stats + 64 > h->stage_bytes) {
     if (h->stage) cudaFree(h->stage);
     h->stage = nullptr;
     h->stage_bytes = 0;
-    if (cudaMalloc(&h->stage, off) != cudaSuccess) return IC_ERR_OOM;
-    h->stage_bytes = off;
+    if (cudaMalloc(&h->stage, o_stats + 64) != cudaSuccess) return IC_ERR_OOM;
+    h->stage_bytes = o_stats + 64;
   }
-  char* g = (char*)h->stage;
+  if (chunk + 1 > h->tb_cap) {
+    if (h->tb_pinned) cudaFreeHost(h->tb_pinned);
+    h->tb_pinned = nullptr;
+    h->tb_cap = 0;
+    if (cudaMallocHost(&h->tb_pinned, 3 * (chunk + 1) * 8) != cudaSuccess) return IC_ERR_OOM;
+    h->tb_cap = chunk + 1;
+  }
+  char* g0 = (char*)h->stage;
   cudaStream_t user = (cudaStream_t)cuda_stream;
-  cudaEvent_t* ev = h->ev;
-  bool ok = cudaEventRecord(ev[48], user) == cudaSuccess &&
-            cudaStreamWaitEvent(h->s_in, ev[48], 0) == cudaSuccess &&
-            cudaStreamWaitEvent(h->s_comp, ev[48], 0) == cudaSuccess;
-  if (out->stats) ok = ok && cudaMemsetAsync(g + o_stats, 0, 64, h->s_comp) == cudaSuccess;
-  const int64_t nch = B >= 16 * 256 ? 16 : (B + 255) / 256;
-  for (int64_t j = 0; j < nch && ok; ++j) {
-    const int64_t b0 = B * j / nch, b1 = B * (j + 1) / nch;
-    const int64_t t0 = tbh[b0], t1 = tbh[b1], nt = t1 - t0;
-    if (t1 < t0) return IC_ERR_INVALID_ARG;
-    cudaEvent_t e_in = ev[(j % 16) * 3], e_k = ev[(j % 16) * 3 + 1];
+  cudaEvent_t* ev = h->ev;  // [slot*4 + 0] inputs staged, +1 kernel done, +2 outputs drained; [12], [13]
+  bool ok = cudaEventRecord(ev[13], user) == cudaSuccess &&
+            cudaStreamWaitEvent(h->s_in, ev[13], 0) == cudaSuccess &&
+            cudaStreamWaitEvent(h->s_comp, ev[13], 0) == cudaSuccess;
+  if (out->stats) ok = ok && cudaMemsetAsync(g0 + o_stats, 0, 64, h->s_comp) == cudaSuccess;
+  int64_t j = 0;
+  for (int64_t b0 = 0; b0 < B && ok; b0 += chunk, ++j) {
+    const int64_t b1 = b0 + chunk < B ? b0 + chunk : B, nbi = b1 - b0;
+    const int64_t t0 = tbh[b0], nt = tbh[b1] - t0;
+    const int sl = (int)(j % 3);
+    char* g = g0 + sl * slot;
+    if (j >= 3) {  // slot reuse: its previous chunk's outputs must be drained, its CSR copied
+      if (cudaEventSynchronize(ev[sl * 4 + 2]) != cudaSuccess) return IC_ERR_CUDA;
+      ok = cudaStreamWaitEvent(h->s_in, ev[sl * 4 + 2], 0) == cudaSuccess;
+    }
+    int64_t* tbp = h->tb_pinned + sl * (chunk + 1);
+    for (int64_t b = 0; b <= nbi; ++b) tbp[b] = tbh[b0 + b] - t0;  // rebase onto the slot's rows
     auto h2d = [&](size_t o, const void* src, size_t bytes) {
       return bytes == 0 || cudaMemcpyAsync(g + o, src, bytes, cudaMemcpyHostToDevice, h->s_in) == cudaSuccess;
     };
-    ok = h2d(o_tb + b0 * 8, tbh + b0, (b1 - b0 + 1) * 8) && h2d(o_r + t0 * 4, in->release + t0, nt * 4) &&
-         h2d(o_d + t0 * 4, in->deadline + t0, nt * 4) && h2d(o_m + t0 * 4, in->mand_wcet + t0, nt * 4) &&
-         h2d(o_n + t0, in->n_opt + t0, nt) && h2d(o_mc + t0 * 4, in->mand_conf + t0, nt * 4);
+    ok = ok && h2d(o_tb, tbp, (nbi + 1) * 8) && h2d(o_r, in->release + t0, nt * 4) &&
+         h2d(o_d, in->deadline + t0, nt * 4) && h2d(o_m, in->mand_wcet + t0, nt * 4) &&
+         h2d(o_n, in->n_opt + t0, nt) && h2d(o_mc, in->mand_conf + t0, nt * 4);
     if (st > 0)
-      ok = ok && h2d(o_ow + t0 * st * 4, in->opt_wcet + t0 * st, nt * st * 4) &&
-           h2d(o_og + t0 * st * 4, in->opt_gain + t0 * st, nt * st * 4);
-    ok = ok && cudaEventRecord(e_in, h->s_in) == cudaSuccess &&
-         cudaStreamWaitEvent(h->s_comp, e_in, 0) == cudaSuccess;
+      ok = ok && h2d(o_ow, in->opt_wcet + t0 * st, nt * st * 4) && h2d(o_og, in->opt_gain + t0 * st, nt * st * 4);
+    ok = ok && cudaEventRecord(ev[sl * 4], h->s_in) == cudaSuccess &&
+         cudaStreamWaitEvent(h->s_comp, ev[sl * 4], 0) == cudaSuccess;
     if (!ok) break;
-    ic_batch_in din = {b1 - b0, (const int64_t*)(g + o_tb) + b0, (const int32_t*)(g + o_r),
-                       (const int32_t*)(g + o_d), (const int32_t*)(g + o_m), (const uint8_t*)(g + o_n),
-                       (const int32_t*)(g + o_ow), (const uint32_t*)(g + o_mc), (const int32_t*)(g + o_og)};
-    ic_batch_out dout = {(int8_t*)(g + o_k), (int32_t*)(g + o_s), (int32_t*)(g + o_f),
-                         (int64_t*)(g + o_q) + b0, (int64_t*)(g + o_c) + b0, (double*)(g + o_ct) + b0,
-                         (int32_t*)(g + o_ms) + b0, (uint8_t*)(g + o_st) + b0,
-                         out->stats ? (int64_t*)(g + o_stats) : nullptr};
+    ic_batch_in din = {nbi, (const int64_t*)(g + o_tb), (const int32_t*)(g + o_r), (const int32_t*)(g + o_d),
+                       (const int32_t*)(g + o_m), (const uint8_t*)(g + o_n), (const int32_t*)(g + o_ow),
+                       (const uint32_t*)(g + o_mc), (const int32_t*)(g + o_og)};
+    ic_batch_out dout = {(int8_t*)(g + o_k), (int32_t*)(g + o_s), (int32_t*)(g + o_f), (int64_t*)(g + o_q),
+                         (int64_t*)(g + o_c), (double*)(g + o_ct), (int32_t*)(g + o_ms), (uint8_t*)(g + o_st),
+                         out->stats ? (int64_t*)(g0 + o_stats) : nullptr};
     rc = ic_sched_solve_batch(h, &din, &dout, h->s_comp);
     if (rc != IC_OK) return rc;
-    ok = cudaEventRecord(e_k, h->s_comp) == cudaSuccess && cudaStreamWaitEvent(h->s_out, e_k, 0) == cudaSuccess;
+    ok = cudaEventRecord(ev[sl * 4 + 1], h->s_comp) == cudaSuccess &&
+         cudaStreamWaitEvent(h->s_out, ev[sl * 4 + 1], 0) == cudaSuccess;
     auto d2h = [&](void* dst, size_t o, size_t bytes) {
       return bytes == 0 || cudaMemcpyAsync(dst, g + o, bytes, cudaMemcpyDeviceToHost, h->s_out) == cudaSuccess;
     };
-    ok = ok && d2h(out->kept + t0, o_k + t0, nt) && d2h(out->start + t0, o_s + t0 * 4, nt * 4) &&
-         d2h(out->finish + t0, o_f + t0 * 4, nt * 4) && d2h(out->q_total + b0, o_q + b0 * 8, (b1 - b0) * 8) &&
-         d2h(out->conf_micro + b0, o_c + b0 * 8, (b1 - b0) * 8) &&
-         d2h(out->conf_total + b0, o_ct + b0 * 8, (b1 - b0) * 8) &&
-         d2h(out->makespan + b0, o_ms + b0 * 4, (b1 - b0) * 4) && d2h(out->status + b0, o_st + b0, b1 - b0);
+    ok = ok && d2h(out->kept + t0, o_k, nt) && d2h(out->start + t0, o_s, nt * 4) &&
+         d2h(out->finish + t0, o_f, nt * 4) && d2h(out->q_total + b0, o_q, nbi * 8) &&
+         d2h(out->conf_micro + b0, o_c, nbi * 8) && d2h(out->conf_total + b0, o_ct, nbi * 8) &&
+         d2h(out->makespan + b0, o_ms, nbi * 4) && d2h(out->status + b0, o_st, nbi) &&
+         cudaEventRecord(ev[sl * 4 + 2], h->s_out) == cudaSuccess;
   }
   int64_t stats_dev[8];
   if (ok && out->stats) {
-    ok = cudaEventRecord(ev[47], h->s_comp) == cudaSuccess && cudaStreamWaitEvent(h->s_out, ev[47], 0) == cudaSuccess &&
-         cudaMemcpyAsync(stats_dev, g + o_stats, 64, cudaMemcpyDeviceToHost, h->s_out) == cudaSuccess;
+    ok = cudaEventRecord(ev[12], h->s_comp) == cudaSuccess && cudaStreamWaitEvent(h->s_out, ev[12], 0) == cudaSuccess &&
+         cudaMemcpyAsync(stats_dev, g0 + o_stats, 64, cudaMemcpyDeviceToHost, h->s_out) == cudaSuccess;
   }
   if (cudaStreamSynchronize(h->s_out) != cudaSuccess || !ok) return IC_ERR_CUDA;
   if (out->stats)
