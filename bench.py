@@ -273,6 +273,7 @@ def main():
     if strong:
         id0, id1 = shard_range(cw.n_instances, rank, world)
         n_inst = id1 - id0
+        hash_id0 = id0
         spans = []  # (global id lo, hi) pieces of this rank's shard
         start = 0
         for _, cnt in cw.u_blocks:
@@ -282,6 +283,7 @@ def main():
     elif cw.u_blocks:  # --instances with C5: an equal slice from the start of every U block (profiling)
         per = args.instances // len(cw.u_blocks)
         n_inst = per * len(cw.u_blocks)
+        hash_id0 = 0
         spans, start = [], 0
         for _, cnt in cw.u_blocks:
             spans.append((start + rank * per, start + (rank + 1) * per))
@@ -289,6 +291,7 @@ def main():
     else:
         n_inst = args.instances or cw.n_instances
         id0 = weak_shard(n_inst, rank)[0]
+        hash_id0 = id0
         spans = [(id0, id0 + n_inst)]
     stream = torch.cuda.Stream(dev)
 
@@ -365,6 +368,12 @@ def main():
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = float(tmax.item())
     stats = out["stats"].cpu().numpy()
+    # plans fingerprint: all_reduce(SUM) of an int64 hash keyed by global id;
+    # identical at any GPU count for the strong-scaled C5 sweep
+    from paper_2011_01112_b200.multigpu import result_hash
+    rh = result_hash(out, inputs["task_begin"], hash_id0, cw.n_tasks).reshape(1)
+    if world > 1:
+        dist.all_reduce(rh)
     total_inst = cw.n_instances if strong else n_inst * world
     value = total_inst * args.steps / (ms / 1e3)
 
@@ -427,6 +436,7 @@ def main():
             "clocks": clk_s,
             "kernel": info,
             "stats": dict(zip(pkg.STATS_FIELDS, [int(x) for x in stats])),
+            "result_hash": hex(int(rh.item()) & ((1 << 64) - 1)),
         }
         if e2e:
             line["e2e"] = e2e

@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 
 import gen
 import oracle
-from paper_2011_01112_b200.multigpu import derived_metrics, reduce_stats, shard_range, weak_shard
+from paper_2011_01112_b200.multigpu import derived_metrics, reduce_stats, result_hash, shard_range, weak_shard
 from tests.gpu_util import stats_from
 
 B = 96
@@ -31,12 +31,23 @@ def _free_port():
     return p
 
 
-def _stats_for(lo, hi):
+def _solve(lo, hi):
     cw = gen.CONFIGS["C2"]
     batch = gen.generate(cw, hi - lo, id_offset=lo)
     out = oracle.solve(batch, oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, max_tasks=32,
                                                   max_horizon=1024), oracle.TIME)
+    return batch, out
+
+
+def _stats_for(lo, hi):
+    batch, out = _solve(lo, hi)
     return stats_from(out, batch)
+
+
+def _hash_for(lo, hi):
+    batch, out = _solve(lo, hi)
+    t = {k: torch.from_numpy(out[k]) for k in ("kept", "start", "finish")}
+    return result_hash(t, torch.from_numpy(batch.task_begin), lo)
 
 
 def _worker(rank, world, port, mode, q):
@@ -45,8 +56,10 @@ def _worker(rank, world, port, mode, q):
     lo, hi = shard_range(B, rank, world) if mode == "strong" else weak_shard(B // world, rank)
     st = torch.from_numpy(_stats_for(lo, hi))
     reduce_stats(st)
+    h = _hash_for(lo, hi).reshape(1)
+    dist.all_reduce(h)
     if rank == 0:
-        q.put(st.numpy().tolist())
+        q.put((st.numpy().tolist(), int(h.item())))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -59,12 +72,14 @@ def test_stats_allreduce_world2(mode):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=240)
+    got, h = q.get(timeout=240)
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
     ref = _stats_for(0, B)
     np.testing.assert_array_equal(np.array(got), ref)
+    if mode == "strong":  # same global ids, any sharding -> same fingerprint
+        assert h == int(_hash_for(0, B).item())
     m = derived_metrics(ref)
     assert 0 < m["accuracy"] <= 1 and 0 <= m["miss_rate"] <= 1
 
