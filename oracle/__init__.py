@@ -167,3 +167,37 @@ def check(batch, result: dict, cfg: OracleConfig) -> np.ndarray:
     c, i, oo = _cfg(cfg, batch), _in(batch), _out(o)
     return np.array([lib.or_check(ctypes.byref(c), ctypes.byref(i), ctypes.byref(oo), b)
                      for b in range(batch.n_instances)], np.int64)
+
+
+# ---------------------------------------------------------------- NEXT-3 (stage completion)
+UTIL_GIVEN, UTIL_MAX, UTIL_EXP, UTIL_LIN = 0, 1, 2, 3
+
+
+def predict_next(heuristic: int, r_cur: int, p_cur: int, p_next: int) -> int:
+    """One step of the Max / Exp / Lin utility heuristics, micro-units."""
+    lib = _load()
+    lib.or_predict_next.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
+    lib.or_predict_next.restype = ctypes.c_int64
+    return int(lib.or_predict_next(heuristic, r_cur, p_cur, p_next))
+
+
+def reassign(batch, kept, done, observed, heuristic: int, cfg: OracleConfig = OracleConfig()) -> dict:
+    """Greedy depth reassignment of Eq. 5 after the EDF-current task's stage
+    completion.  kept: current plan [T] int8; done / observed: per instance."""
+    lib = _load()
+    lib.or_reassign_batch.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(_In), ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(_Out),
+                                      ctypes.c_void_p]
+    lib.or_reassign_batch.restype = ctypes.c_int
+    o = _alloc_out(batch)
+    sw = np.zeros(batch.n_instances, np.uint8)
+    kept = np.ascontiguousarray(kept, np.int8)
+    done = np.ascontiguousarray(done, np.int8)
+    observed = np.ascontiguousarray(observed, np.uint32)
+    rc = lib.or_reassign_batch(ctypes.byref(_cfg(cfg, batch)), ctypes.byref(_in(batch)), _p(kept), _p(done),
+                               _p(observed), heuristic, ctypes.byref(_out(o)), _p(sw))
+    if rc != 0:
+        raise ValueError(f"or_reassign_batch failed ({rc})")
+    o["conf_total"] = o["conf_micro"].astype(np.float64) / 1e6
+    o["swapped"] = sw
+    return o

@@ -498,3 +498,166 @@ int or_check(const or_cfg* cfg, const or_in* in, const or_out* out, int64_t b) {
   release_inst(I); free(I);
   return bits;
 }
+
+/* ======================= NEXT-3: stage completion update ============================
+ * Utility prediction (§II-D) and the greedy depth reassignment of Eq. 5
+ * (§II-E), written in the paper's order.  All confidences in micro-units.
+ *
+ * Predict the next stage from the current one:
+ *   Max: R^{L+1} = 1;  Exp: R^{L+1} = R^L + 0.5 (1 - R^L);
+ *   Lin: R^{L+1} = min(1, R^L * P^{L+1} / P^L)   (integer floor in micro-units)
+ * Given (the oracle utility): the instance's own gains are the true increments. */
+enum { OR_UTIL_GIVEN = 0, OR_UTIL_MAX = 1, OR_UTIL_EXP = 2, OR_UTIL_LIN = 3 };
+
+int64_t or_predict_next(int heuristic, int64_t r_cur, int64_t p_cur, int64_t p_next) {
+  if (heuristic == OR_UTIL_MAX) return 1000000;
+  if (heuristic == OR_UTIL_EXP) return r_cur + (1000000 - r_cur) / 2;
+  if (heuristic == OR_UTIL_LIN) {
+    const int64_t v = p_cur > 0 ? r_cur * p_next / p_cur : 1000000;
+    return v < 1000000 ? v : 1000000;
+  }
+  return r_cur;
+}
+
+/* EDF-feasibility of a plan (codes by input index: -1 drop, else kept stages), the
+ * forward schedule of P:L48/P:L90; fills start/finish and returns 1 if every kept
+ * task meets its deadline. */
+static int schedule_plan(const inst_t* I, const int* kept, int64_t* st, int64_t* fi, int64_t* F_out) {
+  int64_t F = 0;
+  int ok = 1;
+  for (int pos = 0; pos < I->n; ++pos) {
+    const int i = I->pi[pos];
+    st[i] = fi[i] = -1;
+    if (kept[i] < 0) continue;
+    const int64_t s = F > I->r[i] ? F : I->r[i];
+    const int64_t f = s + AT(I->C, i, kept[i]);
+    if (f > I->d[i]) ok = 0;
+    st[i] = s;
+    fi[i] = f;
+    F = f;
+  }
+  *F_out = F;
+  return ok;
+}
+
+/* One instance: the current plan `kept_in` (by input index), the EDF-current task J_1
+ * (the first kept task in EDF order) has completed `done` optional stages and shows
+ * confidence `observed`.  Returns the new plan in kept_out; *swapped = 1 if changed. */
+static int reassign_one(const inst_t* I, const int8_t* kept_in, int done, int64_t observed, int heuristic,
+                        int* kept_out, int64_t* Rnew /* [smax+1] J_1's new curve */, int* j1_out,
+                        int* swapped) {
+  const int n = I->n;
+  *swapped = 0;
+  *j1_out = -1;
+  for (int i = 0; i < n; ++i) kept_out[i] = kept_in[i];
+  int p1 = -1;
+  for (int pos = 0; pos < n && p1 < 0; ++pos)
+    if (kept_in[I->pi[pos]] >= 0) p1 = pos;
+  if (p1 < 0) return OR_OK;  /* nothing is running: the plan stands */
+  const int j1 = I->pi[p1];
+  *j1_out = j1;
+  const int l1 = done, l1s = kept_in[j1];
+  if (l1 < 0 || l1 > l1s || observed < 0 || observed > 1000000) return OR_BAD_INPUT;
+  /* J_1's re-predicted curve from the observed confidence ("revisit estimated utility") */
+  for (int k = 0; k <= I->S[j1]; ++k) Rnew[k] = AT(I->R, j1, k);
+  Rnew[l1] = observed;
+  for (int k = l1 + 1; k <= I->S[j1]; ++k) {
+    if (heuristic == OR_UTIL_GIVEN)
+      Rnew[k] = Rnew[k - 1] + (AT(I->R, j1, k) - AT(I->R, j1, k - 1));
+    else
+      Rnew[k] = or_predict_next(heuristic, Rnew[k - 1], AT(I->C, j1, k - 1), AT(I->C, j1, k));
+  }
+  /* "if the updated future utility ... becomes larger, our previous depth assignment still
+   * preserves optimality": no decrease on [l_1, l_1*] keeps the plan */
+  int lower = 0;
+  for (int k = l1; k <= l1s; ++k)
+    if (Rnew[k] < AT(I->R, j1, k)) lower = 1;
+  if (!lower) return OR_OK;
+  /* Eq. 5: the best extension of a later task within J_1's released budget
+   * sum_{l'=l_1+1}^{l_1*} p_{1l'} (reading R19: the extension's own stages l_i*+1..l),
+   * kept EDF-feasible (SPEC S:L217 strengthening).  Ties: earliest EDF position, then
+   * the shallower depth. */
+  const int64_t released = AT(I->C, j1, l1s) - AT(I->C, j1, l1);
+  const int64_t rem_gain = Rnew[l1s] - Rnew[l1];
+  int* plan = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+  int64_t* st = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1) * 2);
+  int64_t* fi = st + (n > 0 ? n : 1);
+  int best_i = -1, best_l = -1;
+  int64_t best_gain = 0;
+  for (int pos = p1 + 1; pos < n; ++pos) {
+    const int i = I->pi[pos];
+    const int ki = kept_in[i];
+    for (int l = ki + 1; l <= I->S[i]; ++l) {
+      const int64_t cost = AT(I->C, i, l) - (ki >= 0 ? AT(I->C, i, ki) : 0);
+      if (cost > released) break;
+      const int64_t gain = AT(I->R, i, l) - (ki >= 0 ? AT(I->R, i, ki) : 0);
+      if (best_i >= 0 && gain <= best_gain) continue;
+      for (int q = 0; q < n; ++q) plan[q] = kept_in[q];
+      plan[j1] = l1;
+      plan[i] = l;
+      int64_t F;
+      if (!schedule_plan(I, plan, st, fi, &F)) continue;
+      best_i = i; best_l = l; best_gain = gain;
+    }
+  }
+  free(plan);
+  free(st);
+  /* "If R_i^{l^} - R_i^{l*} > R_1^{l_1*} - R_1^{l_1}, we replace the depth assignment" */
+  if (best_i >= 0 && best_gain > rem_gain) {
+    kept_out[j1] = l1;
+    kept_out[best_i] = best_l;
+    *swapped = 1;
+  }
+  return OR_OK;
+}
+
+int or_reassign_batch(const or_cfg* cfg, const or_in* in, const int8_t* kept_in, const int8_t* done,
+                      const uint32_t* observed, int heuristic, const or_out* out, uint8_t* swapped) {
+  if (!cfg || !in || !out || !kept_in || !done || !observed || heuristic < 0 || heuristic > 3) return -1;
+  for (int64_t b = 0; b < in->n_instances; ++b) {
+    inst_t* I = (inst_t*)malloc(sizeof(inst_t));
+    prep(cfg, in, b, I);
+    const int64_t lo = in->task_begin[b], n_all = in->task_begin[b + 1] - lo;
+    for (int64_t i = 0; i < n_all; ++i) {
+      out->kept[lo + i] = -1; out->start[lo + i] = -1; out->finish[lo + i] = -1;
+    }
+    int st = OR_BAD_INPUT, sw = 0;
+    int64_t F = 0, conf = 0;
+    if (!I->bad) {
+      int* kept = (int*)malloc(sizeof(int) * (size_t)(I->n > 0 ? I->n : 1));
+      int64_t* Rnew = (int64_t*)malloc(sizeof(int64_t) * (size_t)(I->smax + 1));
+      int64_t* s = (int64_t*)malloc(sizeof(int64_t) * (size_t)(I->n > 0 ? I->n : 1) * 2);
+      int64_t* f = s + (I->n > 0 ? I->n : 1);
+      int j1;
+      for (int i = 0; i < I->n; ++i)
+        if (kept_in[lo + i] < -1 || kept_in[lo + i] > I->S[i]) I->bad = 1;
+      st = I->bad ? OR_BAD_INPUT
+                  : reassign_one(I, kept_in + lo, done[b], observed[b], heuristic, kept, Rnew, &j1, &sw);
+      if (st == OR_OK) {
+        if (!schedule_plan(I, kept, s, f, &F)) st = OR_INFEASIBLE;  /* the given plan was infeasible */
+        for (int i = 0; i < I->n; ++i) {
+          if (kept[i] < 0) continue;
+          out->kept[lo + i] = (int8_t)kept[i];
+          out->start[lo + i] = (int32_t)s[i];
+          out->finish[lo + i] = (int32_t)f[i];
+          conf += (i == j1) ? Rnew[kept[i]] : AT(I->R, i, kept[i]);
+        }
+      }
+      free(kept); free(Rnew); free(s);
+    }
+    if (st != OR_OK) {
+      for (int64_t i = 0; i < n_all; ++i) {
+        out->kept[lo + i] = -1; out->start[lo + i] = -1; out->finish[lo + i] = -1;
+      }
+      F = 0; conf = 0; sw = 0;
+    }
+    out->q_total[b] = 0;
+    out->conf_micro[b] = conf;
+    out->makespan[b] = (int32_t)F;
+    out->status[b] = (uint8_t)st;
+    swapped[b] = (uint8_t)sw;
+    release_inst(I);
+    free(I);
+  }
+  return 0;
+}
