@@ -111,6 +111,37 @@ int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, 
 int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream);
 int ic_sched_destroy(ic_sched* h);
 
+/* ---- Stage completion (NEXT-3; the scheduler's second event) ---------------
+ * After a stage of the EDF-current task J_1 (the first kept task in EDF order) completes,
+ * its future confidences are re-predicted from the observed one:
+ *   IC_UTIL_MAX  R^{L+1} = 1;   IC_UTIL_EXP  R^{L+1} = R^L + (1 - R^L) / 2;
+ *   IC_UTIL_LIN  R^{L+1} = min(1, R^L * P^{L+1} / P^L);
+ *   IC_UTIL_GIVEN  the instance's own gains (the paper's oracle utility)
+ * (integer floor in micro-units).  If no planned depth of J_1 got less valuable, the plan
+ * stands.  Otherwise Eq. 5: among the later EDF tasks i and depths
+ * l > l_i* whose extra WCET fits J_1's released budget sum_{l'=l_1+1}^{l_1*} p_{1l'} and
+ * keep every deadline, take the largest gain R_i^l - R_i^{l_i*} (ties: the
+ * earlier task, then the shallower depth); if it exceeds J_1's remaining predicted gain
+ * R_1^{l_1*} - R_1^{l_1}, J_1 stops at l_1 and task i runs to l.  Dropped tasks count
+ * as l_i* = -1 (R = 0, C = 0).
+ *   upd->kept:     [T] current plan (as ic_sched_solve_batch writes it), device pointer
+ *   upd->done:     [B] optional stages J_1 has completed, 0 <= done <= kept(J_1)
+ *   upd->observed: [B] J_1's confidence observed after them, micro-units <= 1e6
+ * Outputs: the new plan in out (kept/start/finish/makespan/status; conf_micro and
+ * conf_total = the plan's predicted confidence with J_1 on its new curve; q_total = 0),
+ * swapped[B] = 1 where Eq. 5 changed the plan.  Invalid instances or updates get
+ * IC_INST_BAD_INPUT; a given plan that misses a deadline gets IC_INST_INFEASIBLE.
+ * Asynchronous on cuda_stream; device pointers; the handle's limits apply. */
+enum { IC_UTIL_GIVEN = 0, IC_UTIL_MAX = 1, IC_UTIL_EXP = 2, IC_UTIL_LIN = 3 };
+typedef struct {
+  const int8_t* kept;
+  const int8_t* done;
+  const uint32_t* observed;
+  int32_t heuristic;
+} ic_stage_update;
+int ic_sched_reassign_batch(ic_sched* h, const ic_batch_in* in, const ic_stage_update* upd, ic_batch_out* out,
+                            uint8_t* swapped, void* cuda_stream);
+
 /* Launch geometry chosen at create time (for tests, bench and profiling). */
 typedef struct {
   int32_t threads_per_cta, cols_per_thread, ctas_per_sm, grid;

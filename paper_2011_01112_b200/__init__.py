@@ -17,6 +17,7 @@ from .abi import (  # noqa: F401
     IC_OK, IC_ERR_INVALID_ARG, IC_ERR_LIMIT, IC_ERR_CUDA, IC_ERR_OOM,
     IC_DROP_ALLOWED, IC_MANDATORY_ENFORCED,
     IC_INST_OK, IC_INST_INFEASIBLE, IC_INST_BAD_INPUT, IC_INST_LIMIT,
+    IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN,
     INPUT_FIELDS, OUTPUT_FIELDS, STATS_FIELDS,
     SchedConfig, SchedInfo, Scheduler, ICSchedError, lib_path, load_library,
     alloc_inputs, alloc_outputs, gen_batch_device,

@@ -75,7 +75,14 @@ class _GenCfg(ctypes.Structure):
 
 
 EXPORTED = ("ic_sched_create", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
-            "ic_sched_get_info", "ic_gen_batch_device")
+            "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch")
+
+IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
+
+
+class _Upd(ctypes.Structure):
+    _fields_ = [("kept", ctypes.c_void_p), ("done", ctypes.c_void_p), ("observed", ctypes.c_void_p),
+                ("heuristic", ctypes.c_int32)]
 
 _lib = None
 
@@ -100,6 +107,8 @@ def load_library():
         lib.ic_sched_get_info.argtypes = [ctypes.c_void_p, P(SchedInfo)]
         lib.ic_gen_batch_device.argtypes = [P(_GenCfg), ctypes.c_int64, ctypes.c_int64] + \
             [ctypes.c_void_p] * 9
+        lib.ic_sched_reassign_batch.argtypes = [ctypes.c_void_p, P(_In), P(_Upd), P(_Out), ctypes.c_void_p,
+                                                ctypes.c_void_p]
         for f in EXPORTED:
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
@@ -187,6 +196,26 @@ class Scheduler:
                                                  ctypes.c_void_p(stream.cuda_stream))
         if rc != IC_OK:
             raise ICSchedError("ic_sched_solve_batch_host", rc)
+        return outputs
+
+    def reassign_batch(self, inputs: dict, kept, done, observed, heuristic: int = IC_UTIL_EXP,
+                       outputs: dict | None = None, swapped=None, stream=None):
+        """ic_sched_reassign_batch (stage completion, Eq. 5) on CUDA tensors; asynchronous."""
+        import torch
+        if outputs is None:
+            outputs = alloc_outputs(_n_instances(inputs), inputs["release"].numel(),
+                                    device=inputs["release"].device)
+        if swapped is None:
+            swapped = torch.empty(_n_instances(inputs), dtype=torch.uint8, device=inputs["release"].device)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        i, o = self._marshal(inputs, outputs)
+        u = _Upd(_ptr(kept), _ptr(done), _ptr(observed), heuristic)
+        rc = self._lib.ic_sched_reassign_batch(self._h, ctypes.byref(i), ctypes.byref(u), ctypes.byref(o),
+                                               _ptr(swapped), ctypes.c_void_p(stream.cuda_stream))
+        if rc != IC_OK:
+            raise ICSchedError("ic_sched_reassign_batch", rc)
+        outputs["swapped"] = swapped
         return outputs
 
     def close(self):

@@ -308,6 +308,24 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   return IC_OK;
 }
 
+extern "C" int ic_sched_reassign_impl(const ic_sched_config* cfg, int sms, const ic_batch_in* in,
+                                      const ic_stage_update* upd, ic_batch_out* out, uint8_t* swapped,
+                                      void* cuda_stream);
+
+extern "C" int ic_sched_reassign_batch(ic_sched* h, const ic_batch_in* in, const ic_stage_update* upd,
+                                       ic_batch_out* out, uint8_t* swapped, void* cuda_stream) {
+  if (!h || !upd || !swapped) return IC_ERR_INVALID_ARG;
+  int rc = check_io(in, out);
+  if (rc != IC_OK) return rc;
+  if (in->n_instances == 0) return IC_OK;
+  if (!upd->kept || !upd->done || !upd->observed || upd->heuristic < IC_UTIL_GIVEN ||
+      upd->heuristic > IC_UTIL_LIN)
+    return IC_ERR_INVALID_ARG;
+  if (h->cfg.max_opt_stages > 0 && (!in->opt_wcet || !in->opt_gain)) return IC_ERR_INVALID_ARG;
+  if (cudaSetDevice(h->cfg.device) != cudaSuccess) return IC_ERR_CUDA;
+  return ic_sched_reassign_impl(&h->cfg, h->sms, in, upd, out, swapped, cuda_stream);
+}
+
 // Host-buffer entry point: H2D of the inputs, solve, D2H of the outputs.  The batch
 // is cut into instance chunks (>= 8, each <= ~256 MB staged) that cycle through a
 // ring of three device staging slots over three internal streams (copy-in,

@@ -281,3 +281,43 @@ def test_reward_axis_paper_delta(monkeypatch, name, mode):
         got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
                         delta=100_000)
         assert_parity(got, ref, f"{name} axis={axis} mode={mode}")
+
+
+@pytest.mark.parametrize("heuristic", [0, 1, 2, 3])
+@pytest.mark.parametrize("shape", ["tiny", "C2", "C3"])
+def test_reassign_vs_oracle(heuristic, shape):
+    """NEXT-3: stage-completion reassignment (Eq. 5) on the GPU against the oracle."""
+    import paper_2011_01112_b200 as pkg
+    from tests.gpu_util import to_device
+    rng = np.random.default_rng(50 + heuristic)
+    if shape == "tiny":
+        batch = gen.tiny_random(rng, 4000, max_tasks=6, max_opt=3, horizon=30)
+        mt, mo, H = 6, 3, 30
+    else:
+        cw = gen.CONFIGS[shape]
+        batch = gen.generate(cw, 2000 if shape == "C2" else 300)
+        mt, mo, H = cw.n_tasks, cw.n_opt, cw.horizon
+    ocfg = OracleConfig(delta_micro=100_000, max_tasks=mt, max_horizon=H)
+    plan = oracle.solve(batch, ocfg, TIME)
+    done = np.zeros(batch.n_instances, np.int8)
+    obs = np.zeros(batch.n_instances, np.uint32)
+    from oracle import definition
+    for b in range(batch.n_instances):
+        lo, hi = batch.task_begin[b], batch.task_begin[b + 1]
+        k = plan["kept"][lo:hi]
+        first = [i for i in definition.edf_order(definition.tasks_from_batch(batch, b)) if k[i] >= 0]
+        if first:
+            done[b] = rng.integers(0, k[first[0]] + 1)
+            obs[b] = rng.integers(0, 101) * 10_000
+    ref = oracle.reassign(batch, plan["kept"], done, obs, heuristic, ocfg)
+    sc = pkg.SchedConfig(max_tasks=mt, max_opt_stages=mo, max_horizon=H, delta_micro=100_000)
+    with pkg.Scheduler(sc) as s:
+        dev = to_device(batch)
+        out = s.reassign_batch(dev, torch.from_numpy(plan["kept"]).cuda(), torch.from_numpy(done).cuda(),
+                               torch.from_numpy(obs).cuda(), heuristic)
+        torch.cuda.synchronize()
+    got = {k: v.cpu().numpy() for k, v in out.items()}
+    for k in ("kept", "start", "finish", "conf_micro", "makespan", "status", "swapped"):
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+    if heuristic != 1:
+        assert got["swapped"].sum() > 0
