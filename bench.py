@@ -235,6 +235,57 @@ def run_reference(args, cw, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_reassign(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong):
+    """--op reassign: one stage-completion update per instance of the solved batch (J_1 after its
+    mandatory block with a uniformly random observed confidence, Exp re-prediction)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2011_01112_b200 as pkg
+    with torch.cuda.stream(stream):
+        sched.solve_batch(inputs, out, stream)
+        kept = out["kept"].clone()
+        g = torch.Generator(device=dev).manual_seed(cw.seed)
+        done = torch.zeros(n_inst, dtype=torch.int8, device=dev)
+        observed = torch.randint(0, 1_000_001, (n_inst,), generator=g, device=dev).to(torch.uint32)
+        out2 = pkg.alloc_outputs(n_inst, kept.numel(), device=dev)
+        sw = torch.empty(n_inst, dtype=torch.uint8, device=dev)
+        for _ in range(args.warmup):
+            sched.reassign_batch(inputs, kept, done, observed, pkg.IC_UTIL_EXP, out2, sw, stream)
+    stream.synchronize()
+    k = args.steps or 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk, torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(k):
+            sched.reassign_batch(inputs, kept, done, observed, pkg.IC_UTIL_EXP, out2, sw, stream)
+        e1.record(stream)
+        e1.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    if rank == 0:
+        total = cw.n_instances if strong else n_inst * world
+        per_ms = ms / k
+        in_bytes = sum(v.numel() * v.element_size() for v in inputs.values()) / n_inst
+        io = in_bytes + 9 * inputs["release"].numel() / n_inst + 32  # descriptors + plan in/out + per-instance
+        achieved = io * n_inst / (per_ms / 1e3) / 1e9
+        peak = _peaks().get("hbm_gbs", 6553.3)
+        print(json.dumps({
+            "metric": "stage-completion updates/sec (Eq. 5 greedy reassignment)", "value": total * k / (ms / 1e3),
+            "unit": "updates/s", "n_gpus": world, "steps": k, "warmup": args.warmup, "ms_per_step": per_ms,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic (device-generated, seeded)",
+            "config": workload_config(cw, args, n_inst),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "work": "descriptor + plan bytes per instance (one read, one write)"},
+            "gpu_launches": k, "clocks": clk.summary(),
+            "swapped_fraction": float(sw.float().mean().item()),
+        }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -246,6 +297,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--op", default="solve", choices=["solve", "reassign"],
+                    help="reassign: time the stage-completion update (NEXT-3, Eq. 5) on the solved batch")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -328,6 +381,13 @@ def main():
         out["stats"].zero_()
         sched.solve_batch(inputs, out, stream)
         reduce_stats(out["stats"])
+
+    if args.op == "reassign":
+        run_reassign(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong)
+        sched.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):

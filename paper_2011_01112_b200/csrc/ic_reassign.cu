@@ -177,16 +177,26 @@ __global__ void __launch_bounds__(256) reassign_kernel(const RParams p) {
         ck[pos] = c;
       }
       __syncwarp();
+      int norel = 1;
+      for (int pos = lane; pos < n; pos += 32) norel &= rr[pos] == 0;
+      norel = __all_sync(0xffffffffu, norel);
       if (lane == 0) {
         long long F = 0;
         for (int pos = 0; pos < n; ++pos) {
           fb[pos] = (int)F;
           if (ck[pos] >= 0) F = max(F, (long long)rr[pos]) + ck[pos];
         }
+        if (norel) {  // suffix minimum slack of the truncated schedule (reuses ord: no longer needed)
+          long long smin = 1ll << 40;
+          for (int pos = n - 1; pos >= 0; --pos) {
+            ord[pos] = (int)min(smin, (long long)(1 << 30));
+            if (ck[pos] >= 0) smin = min(smin, (long long)dd[pos] - (fb[pos] + ck[pos]));
+          }
+        }
       }
       __syncwarp();
       for (int pos = p1 + 1 + lane; pos < n; pos += 32) {
-        const int i = ord[pos];
+        const int i = (int)(key[pos] & 0xFFF);
         const int64_t t = lo + i;
         const int S = in.n_opt[t], ki = p.kept_in[t];
         long long C = in.mand_wcet[t], R = in.mand_conf[t], C0 = 0, R0 = 0;
@@ -206,10 +216,14 @@ __global__ void __launch_bounds__(256) reassign_kernel(const RParams p) {
           // EDF feasibility of the plan with J_1 truncated and task i at depth l
           long long F = max((long long)fb[pos], (long long)rr[pos]) + C;
           bool ok = F <= dd[pos];
-          for (int q = pos + 1; q < n && ok; ++q) {
-            if (ck[q] < 0) continue;
-            F = max(F, (long long)rr[q]) + ck[q];
-            ok = F <= dd[q];
+          if (norel) {  // no releases: every later finish moves by exactly the delay
+            ok = ok && F - (ki >= 0 ? (long long)fb[pos] + ck[pos] : (long long)fb[pos]) <= ord[pos];
+          } else {
+            for (int q = pos + 1; q < n && ok; ++q) {
+              if (ck[q] < 0) continue;
+              F = max(F, (long long)rr[q]) + ck[q];
+              ok = F <= dd[q];
+            }
           }
           if (!ok) continue;
           const unsigned long long kv = ((unsigned long long)(gain + (1ll << 31)) << 32) |
