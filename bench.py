@@ -235,6 +235,49 @@ def run_reference(args, cw, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_replan(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong):
+    """--op replan: every instance's last task arrives; the rows before its EDF position come from
+    the state of the solve without it (Alg. 1 from row k).  Reported beside a full solve."""
+    import torch
+    import torch.distributed as dist
+    N = cw.n_tasks
+    base = {k: (v.view(n_inst, N, -1)[:, :N - 1].reshape(n_inst * (N - 1), -1).squeeze(-1).contiguous()
+                if k != "task_begin" else torch.arange(n_inst + 1, device=dev, dtype=torch.int64) * (N - 1))
+            for k, v in inputs.items()}
+    base["opt_wcet"] = base["opt_wcet"].view(-1, cw.n_opt)
+    base["opt_gain"] = base["opt_gain"].view(-1, cw.n_opt)
+    state = torch.empty(sched.state_bytes(n_inst), dtype=torch.uint8, device=dev)
+    k = args.steps or 10
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            sched.solve_batch(inputs, out, stream)
+        ev[0].record(stream)
+        for _ in range(k):
+            sched.solve_batch(inputs, out, stream)
+        ev[1].record(stream)
+        tr = 0.0
+        for _ in range(k):
+            sched.solve_batch_state(base, state, None, stream)
+            ev[2].record(stream)
+            sched.replan_batch(inputs, state, out, stream)
+            ev[3].record(stream)
+            ev[3].synchronize()
+            tr += ev[2].elapsed_time(ev[3])
+    stream.synchronize()
+    full_ms = ev[0].elapsed_time(ev[1]) / k
+    rep_ms = tr / k
+    if rank == 0:
+        total = n_inst * world
+        print(json.dumps({
+            "metric": "re-plans on arrival/sec (Alg. 1 from row k)", "value": total / (rep_ms / 1e3),
+            "unit": "instances/s", "n_gpus": world, "steps": k, "warmup": args.warmup, "ms_per_step": rep_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (device-generated, seeded)", "config": workload_config(cw, args, n_inst),
+            "full_solve_ms": full_ms, "speedup_vs_full_solve": full_ms / rep_ms, "gpu_launches": 2 * k}),
+            flush=True)
+
+
 def run_reassign(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong):
     """--op reassign: one stage-completion update per instance of the solved batch (J_1 after its
     mandatory block with a uniformly random observed confidence, Exp re-prediction)."""
@@ -297,8 +340,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--op", default="solve", choices=["solve", "reassign"],
-                    help="reassign: time the stage-completion update (NEXT-3, Eq. 5) on the solved batch")
+    ap.add_argument("--op", default="solve", choices=["solve", "reassign", "replan"],
+                    help="reassign: the stage-completion update (NEXT-3, Eq. 5) on the solved batch; replan: "
+                         "one arrival per instance re-planned from its row (NEXT-2, needs --delta-micro)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -382,6 +426,12 @@ def main():
         sched.solve_batch(inputs, out, stream)
         reduce_stats(out["stats"])
 
+    if args.op == "replan":
+        run_replan(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong)
+        sched.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.op == "reassign":
         run_reassign(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong)
         sched.close()

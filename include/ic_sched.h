@@ -142,6 +142,32 @@ typedef struct {
 int ic_sched_reassign_batch(ic_sched* h, const ic_batch_in* in, const ic_stage_update* upd, ic_batch_out* out,
                             uint8_t* swapped, void* cuda_stream);
 
+/* ---- Incremental re-plan on arrival (NEXT-2; Alg. 1 from row k) -------
+ * "When a task J_k arrives whose deadline is d_k, existing table rows for tasks with
+ * deadlines d < d_k stay the same.  Table rows for tasks with deadlines d >= d_k
+ * (including the new arrival) need to be (re)computed".  With a state buffer
+ * the solver keeps every DP row of each instance (active columns + tail value), its
+ * decisions and tail codes:
+ *   ic_sched_state_bytes(h, B)        bytes of state for B instances (caller allocates,
+ *                                     device memory, 256-byte aligned)
+ *   ic_sched_solve_batch_state(...)   = ic_sched_solve_batch, and fills the state
+ *   ic_sched_replan_batch(...)        the inputs are the previous instances with ONE new
+ *                                     task appended at the end of each instance (every
+ *                                     other task unchanged and in the same order); rows
+ *                                     before the arrival's EDF position are taken from the
+ *                                     state, the rest recomputed; the state is updated, so
+ *                                     arrivals can be chained.  Results are identical to a
+ *                                     full ic_sched_solve_batch of the new instances.
+ * Requires a fixed Delta (delta_micro > 0: the FPTAS step eps*R/N changes with N) and
+ * max_horizon <= 16384 (IC_ERR_INVALID_ARG / IC_ERR_LIMIT otherwise).  Every ckpt-th row
+ * is kept (IC_SCHED_CKPT, default 4), so a re-plan restarts at the last kept row before the
+ * arrival; if the instance's sweep axis changes (time vs reward) it restarts at row 0.
+ * Same stream/ownership rules as ic_sched_solve_batch. */
+int64_t ic_sched_state_bytes(const ic_sched* h, int64_t n_instances);
+int ic_sched_solve_batch_state(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* state,
+                               void* cuda_stream);
+int ic_sched_replan_batch(ic_sched* h, const ic_batch_in* in, void* state, ic_batch_out* out, void* cuda_stream);
+
 /* Launch geometry chosen at create time (for tests, bench and profiling). */
 typedef struct {
   int32_t threads_per_cta, cols_per_thread, ctas_per_sm, grid;

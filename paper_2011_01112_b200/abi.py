@@ -75,7 +75,8 @@ class _GenCfg(ctypes.Structure):
 
 
 EXPORTED = ("ic_sched_create", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
-            "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch")
+            "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch", "ic_sched_state_bytes",
+            "ic_sched_solve_batch_state", "ic_sched_replan_batch")
 
 IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
 
@@ -109,8 +110,13 @@ def load_library():
             [ctypes.c_void_p] * 9
         lib.ic_sched_reassign_batch.argtypes = [ctypes.c_void_p, P(_In), P(_Upd), P(_Out), ctypes.c_void_p,
                                                 ctypes.c_void_p]
+        lib.ic_sched_solve_batch_state.argtypes = [ctypes.c_void_p, P(_In), P(_Out), ctypes.c_void_p,
+                                                   ctypes.c_void_p]
+        lib.ic_sched_replan_batch.argtypes = [ctypes.c_void_p, P(_In), ctypes.c_void_p, P(_Out), ctypes.c_void_p]
+        lib.ic_sched_state_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         for f in EXPORTED:
             getattr(lib, f).restype = ctypes.c_int
+        lib.ic_sched_state_bytes.restype = ctypes.c_int64
         _lib = lib
     return _lib
 
@@ -216,6 +222,39 @@ class Scheduler:
         if rc != IC_OK:
             raise ICSchedError("ic_sched_reassign_batch", rc)
         outputs["swapped"] = swapped
+        return outputs
+
+    def state_bytes(self, n_instances: int) -> int:
+        """Device bytes of re-plan state for n_instances (ic_sched_state_bytes)."""
+        v = self._lib.ic_sched_state_bytes(self._h, n_instances)
+        if v < 0:
+            raise ICSchedError("ic_sched_state_bytes", int(v))
+        return int(v)
+
+    def solve_batch_state(self, inputs: dict, state, outputs: dict | None = None, stream=None) -> dict:
+        """ic_sched_solve_batch_state: solve and keep every DP row in `state` (uint8 CUDA tensor)."""
+        return self._state_call("ic_sched_solve_batch_state", inputs, state, outputs, stream)
+
+    def replan_batch(self, inputs: dict, state, outputs: dict | None = None, stream=None) -> dict:
+        """ic_sched_replan_batch: each instance gained one task (appended last); re-plan from its row."""
+        return self._state_call("ic_sched_replan_batch", inputs, state, outputs, stream)
+
+    def _state_call(self, fn, inputs, state, outputs, stream):
+        import torch
+        if outputs is None:
+            outputs = alloc_outputs(_n_instances(inputs), inputs["release"].numel(),
+                                    device=inputs["release"].device)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        i, o = self._marshal(inputs, outputs)
+        if fn == "ic_sched_replan_batch":
+            rc = self._lib.ic_sched_replan_batch(self._h, ctypes.byref(i), _ptr(state), ctypes.byref(o),
+                                                 ctypes.c_void_p(stream.cuda_stream))
+        else:
+            rc = self._lib.ic_sched_solve_batch_state(self._h, ctypes.byref(i), ctypes.byref(o), _ptr(state),
+                                                      ctypes.c_void_p(stream.cuda_stream))
+        if rc != IC_OK:
+            raise ICSchedError(fn, rc)
         return outputs
 
     def close(self):

@@ -237,8 +237,52 @@ static int check_io(const ic_batch_in* in, const ic_batch_out* out) {
   return IC_OK;
 }
 
+static int state_ckpt() {  // checkpoint every c-th DP row (power of two; IC_SCHED_CKPT overrides)
+  int c = env_int("IC_SCHED_CKPT", 4);
+  return c >= 1 && (c & (c - 1)) == 0 ? c : 4;
+}
+static int64_t state_rows_bytes(const ic_sched* h) {
+  return (int64_t)(h->cfg.max_tasks / state_ckpt() + 1) * (h->cfg.max_horizon + 1) * 4;
+}
+static int64_t state_dec_bytes(const ic_sched* h) { return (int64_t)h->cfg.max_tasks * h->L.nq * 32 * h->nw * 4; }
+static int64_t state_stride(const ic_sched* h) {
+  return (state_rows_bytes(h) + state_dec_bytes(h) + (int64_t)(h->cfg.max_tasks + 1) * 4 + 255) & ~(int64_t)255;
+}
+
+static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream, void* state,
+                        int replan);
+
 extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch_out* out,
                                     void* cuda_stream) {
+  return launch_solve(h, in, out, cuda_stream, nullptr, 0);
+}
+
+extern "C" int64_t ic_sched_state_bytes(const ic_sched* h, int64_t n_instances) {
+  if (!h || n_instances < 0) return IC_ERR_INVALID_ARG;
+  return state_stride(h) * n_instances;
+}
+
+static int state_ok(const ic_sched* h, const void* state) {
+  if (!h || !state) return IC_ERR_INVALID_ARG;
+  if (h->cfg.delta_micro == 0) return IC_ERR_INVALID_ARG;  // FPTAS Delta changes with every arrival
+  if (h->sb) return IC_ERR_LIMIT;                          // in-place rows (H > 16384) keep no state
+  return IC_OK;
+}
+
+extern "C" int ic_sched_solve_batch_state(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* state,
+                                          void* cuda_stream) {
+  const int rc = state_ok(h, state);
+  return rc != IC_OK ? rc : launch_solve(h, in, out, cuda_stream, state, 0);
+}
+
+extern "C" int ic_sched_replan_batch(ic_sched* h, const ic_batch_in* in, void* state, ic_batch_out* out,
+                                     void* cuda_stream) {
+  const int rc = state_ok(h, state);
+  return rc != IC_OK ? rc : launch_solve(h, in, out, cuda_stream, state, 1);
+}
+
+static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream, void* state,
+                        int replan) {
   if (!h) return IC_ERR_INVALID_ARG;
   int rc = check_io(in, out);
   if (rc != IC_OK) return rc;
@@ -298,6 +342,12 @@ extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch
   p.off_aux = L.off_aux;
   p.off_sQ = L.off_sQ;
   p.axis_mode = env_int("IC_SCHED_AXIS", 0);
+  p.state = (char*)state;
+  p.state_stride = state_stride(h);
+  p.state_dec_off = state_rows_bytes(h);
+  p.state_tail_off = state_rows_bytes(h) + state_dec_bytes(h);
+  p.replan = replan;
+  p.ckpt = state_ckpt();
   p.work = h->work;
   p.ndec = L.ndec;
   p.dec_words = (int64_t)h->cfg.max_tasks * L.nq * 32 * h->nw;

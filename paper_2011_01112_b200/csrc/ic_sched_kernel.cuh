@@ -70,9 +70,25 @@ struct Params {
   int cap;     // row buffer capacity in columns (32 NW x COLS)
   int off_aux, off_sQ;
   int axis_mode;  // 0 auto (per instance), 1 time axis only, 2 reward axis whenever eligible
+  // NEXT-2 (incremental re-plan): per-instance state = every DP row (its active
+  // columns and tail value, stride H+1), the decisions and the tail nibbles
+  char* state;
+  int64_t state_stride, state_dec_off, state_tail_off;
+  int replan;  // 1: the last task of each instance is a new arrival; rows before it are kept
+  int ckpt;    // rows kept in the state: every ckpt-th (rows ckpt-1, 2 ckpt-1, ...), power of two
   unsigned long long* work;  // [2] dynamic instance counter, CTAs finished (reset by the last CTA)
   int rowbuf_stride;  // ints per row buffer (pad + capacity)
 };
+
+__device__ __forceinline__ int32_t* state_rows(const Params& p, int64_t b) {
+  return (int32_t*)(p.state + b * p.state_stride);
+}
+__device__ __forceinline__ uint32_t* state_dec(const Params& p, int64_t b) {
+  return (uint32_t*)(p.state + b * p.state_stride + p.state_dec_off);
+}
+__device__ __forceinline__ int32_t* state_tail(const Params& p, int64_t b) {
+  return (int32_t*)(p.state + b * p.state_stride + p.state_tail_off);
+}
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -471,7 +487,8 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
   // a4 axis: the paper's reward-indexed table (Eqs. 1-2) when it is the smaller sweep
   // (e.g. Delta = 0.1), else its time-indexed dual.  Releases need the
   // budget-tracked backtrack, so they stay on the time axis.
-  const bool rw = p.axis_mode != 1 && !anyrel && qcarry + 1 <= p.cap && (p.axis_mode == 2 || wr < wt);
+  const bool rw = p.axis_mode != 1 && !anyrel && qcarry + 1 <= p.cap && (!p.state || qcarry < p.H) &&
+                 (p.axis_mode == 2 || wr < wt);
   if (rw) {
     for (int pos = lane; pos < n; pos += 32) {
       int4* f = S.info + s * p.max_tasks + pos;
@@ -490,6 +507,18 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     mi[7] = S.info[s * p.max_tasks].x;
     mi[8] = S.info[s * p.max_tasks + n - 1].x;
     mi[9] = rw ? 1 : 0;
+    mi[10] = 0;
+  }
+  if (p.replan) {  // the arrival is the instance's last task: rows before its EDF position stand
+    int k = 0;
+    for (int pos = lane; pos < n; pos += 32)
+      if ((int)(S.key[pos] & 0xFFF) == n - 1) k = pos;
+    k = __reduce_max_sync(0xffffffffu, k);
+    k = k / p.ckpt * p.ckpt;  // restart after the last checkpointed row before the arrival
+    const int32_t* st = state_tail(p, b);
+    if (st[p.max_tasks] != (rw ? 1 : 0)) k = 0;  // the sweep axis changed: nothing to reuse
+    for (int pos = lane; pos < k; pos += 32) S.tail[s * p.max_tasks + pos] = st[pos];
+    if (lane == 0) S.misc[s * 16 + 10] = k;
   }
   __syncwarp();
   return ST_OK;
@@ -514,7 +543,8 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
           nib = S.tail[s * p.max_tasks + pos];
         } else {
           const int g = t / NT, l = t - g * NT;
-          const uint32_t w = S.dec[db * p.dec_words + ((size_t)pos * p.nq + (g >> 3)) * NT + l];
+          const uint32_t* dbase = p.state ? state_dec(p, mi[2]) : S.dec + db * p.dec_words;
+          const uint32_t w = dbase[((size_t)pos * p.nq + (g >> 3)) * NT + l];
           nib = (int)((w >> (4 * (g & 7))) & 15u);
         }
         if (rw) {  // reward axis: the nibble is the code; step to column r - q
@@ -720,6 +750,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     const int n = (int)mi[0];
     const int d_first = (int)mi[7];
     const bool rw = mi[9] != 0;
+    const int64_t bcur = mi[2];
+    const int k0 = p.replan ? (int)mi[10] : 0;  // first row to (re)compute
+    if (p.state) {
+      decb = state_dec(p, bcur);
+      if (tid == 0) state_tail(p, bcur)[p.max_tasks] = rw ? 1 : 0;
+    }
     if ((int)rw != padmode) {  // the pad left of column 0 must read as "invalid" for this axis
       padmode = rw;
       for (int bb = 0; bb < (SB ? 1 : 2); ++bb)
@@ -736,14 +772,25 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     const int2* rpb = S.rowp + (size_t)s * p.max_tasks * p.kp;
     const int32_t* auxp = S.aux + s * p.max_tasks;
     int M = 15;
-    int4 f = inf[0];
-    int32_t* const tailp = S.tail + s * p.max_tasks;
-    const int2* ops = rpb;
-    uint32_t* decrow = decb;
     const size_t dec_row_words = (size_t)p.nq * NT;
     const int kp = p.kp;
+    const int64_t rstride = p.H + 1;
+    if (k0 > 0) {  // restore row k0-1 (its active columns, then its tail value up to d_k0)
+      const int32_t* srow = state_rows(p, bcur) + (int64_t)(k0 / p.ckpt - 1) * rstride;
+      int32_t* dst = buf0 + (k0 & 1) * RSb;
+      const int dprev = inf[k0 - 1].x, dk = inf[k0].x;  // deadlines, or Qpre on the reward axis
+      M = srow[p.H];
+      for (int t = tid; t <= dprev; t += NT) dst[t] = srow[t];
+      const int first = dprev + 1 > 0 ? dprev + 1 : 0;
+      for (int t = first + ((tid - first) & (NT - 1)); t <= dk; t += NT) dst[t] = rw ? INFV : M;
+      bar_sync(BAR_DP, NT);
+    }
+    int4 f = inf[k0];
+    int32_t* const tailp = S.tail + s * p.max_tasks;
+    const int2* ops = rpb + (size_t)k0 * kp;
+    uint32_t* decrow = decb + (size_t)k0 * dec_row_words;
 #pragma unroll 1
-    for (int pos = 0; pos < n; ++pos) {
+    for (int pos = k0; pos < n; ++pos) {
       const int4 fn = pos + 1 < n ? inf[pos + 1] : f;  // next row's header, off the critical path
       const int d = f.x, K = f.y & 255, r = f.z, dn = f.w;
       const bool gen = (f.y >> 8) & 1;
@@ -757,6 +804,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
           const int first = d + 1;
 #pragma unroll 1
           for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = INFV;
+        }
+        if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
+          int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
+          for (int t = tid; t <= d; t += NT) srow[t] = nxt[t];
         }
       } else {
         // admit value at column d: every column t > d shares it (tail collapse).  In
@@ -781,6 +832,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
           for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = Mn;
         }
         M = Mn;
+        if (p.state) {  // keep checkpoint rows for later re-plans: active columns, tail value
+          if (((pos + 1) & (p.ckpt - 1)) == 0) {
+            int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
+            for (int t = tid; t <= d; t += NT) srow[t] = nxt[t];
+            if (tid == 0) srow[p.H] = Mn;
+          }
+          if (tid == 0) state_tail(p, bcur)[pos] = Mv & 15;
+        }
       }
       f = fn;
       ops += kp;

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared(header):
     txt = open(os.path.join(ROOT, "include", header)).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return set(re.findall(r"^\s*int\s+(ic_\w+)\s*\(", txt, flags=re.M))
+    return set(re.findall(r"^\s*(?:int|int64_t)\s+(ic_\w+)\s*\(", txt, flags=re.M))
 
 
 def test_library_exports_every_declared_symbol():

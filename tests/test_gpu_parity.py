@@ -321,3 +321,52 @@ def test_reassign_vs_oracle(heuristic, shape):
         np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
     if heuristic != 1:
         assert got["swapped"].sum() > 0
+
+
+def _first_tasks(batch, counts):
+    """Per instance b keep its first counts[b] tasks (a task set before later arrivals)."""
+    from gen import Batch
+    parts = []
+    for b in range(batch.n_instances):
+        one = batch.instance(b)
+        m = int(counts[b])
+        parts.append(Batch(np.array([0, m], np.int64), one.release[:m], one.deadline[:m], one.mand_wcet[:m],
+                           one.n_opt[:m], one.opt_wcet[:m], one.mand_conf[:m], one.opt_gain[:m]))
+    return gen.concat(parts, batch.opt_stride)
+
+
+@pytest.mark.parametrize("ckpt", ["1", "4"])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("shape", ["C2", "tiny"])
+def test_incremental_replan(monkeypatch, shape, mode, ckpt):
+    """NEXT-2 (Alg. 1 from row k): chained arrivals re-planned from the
+    state equal a full solve of the grown task set (GPU and oracle)."""
+    import paper_2011_01112_b200 as pkg
+    from tests.gpu_util import to_device
+    monkeypatch.setenv("IC_SCHED_CKPT", ckpt)
+    rng = np.random.default_rng(70 + mode)
+    if shape == "C2":
+        cw = gen.WorkloadConfig("C2x", 0, 34, 4, 1024, 0.6, 1.0, 35, 0x2011011102)
+        full = gen.generate(cw, 400)
+        mt, mo, H = 34, 4, 1024
+        base = np.full(full.n_instances, 31)
+    else:
+        full = gen.tiny_random(rng, 2000, max_tasks=7, max_opt=3, horizon=40)
+        mt, mo, H = 7, 3, 40
+        sizes = np.diff(full.task_begin)
+        keep = sizes >= 3
+        full = full.select(np.nonzero(keep)[0])
+        base = np.diff(full.task_begin) - 3
+    sc = pkg.SchedConfig(max_tasks=mt, max_opt_stages=mo, max_horizon=H, delta_micro=100_000, drop_mode=mode)
+    with pkg.Scheduler(sc) as s:
+        state = torch.zeros(s.state_bytes(full.n_instances), dtype=torch.uint8, device="cuda")
+        b0 = _first_tasks(full, base)
+        s.solve_batch_state(to_device(b0), state)
+        for add in (1, 2, 3):
+            bk = _first_tasks(full, base + add)
+            out = s.replan_batch(to_device(bk), state)
+            torch.cuda.synchronize()
+            got = {k: v.cpu().numpy() for k, v in out.items()}
+            ref = oracle.solve(bk, OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=mt, max_horizon=H),
+                               TIME)
+            assert_parity(got, ref, f"{shape} arrival {add} mode={mode}")
