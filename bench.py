@@ -329,6 +329,39 @@ def run_reassign(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev,
         }), flush=True)
 
 
+def run_simulate(args, rank, world, local):
+    """--op simulate (NEXT-4): many independent edge servers (P:L345-356 load sweep shape) in
+    lockstep; every round batches all servers' re-plans into one host-buffer GPU solve.  The
+    line reports the planner's throughput and the four policies' accuracy / miss rate."""
+    import torch
+    import torch.distributed as dist
+    import paper_2011_01112_b200 as pkg
+    servers = args.instances or 2048
+    kw = dict(servers=servers, clients=args.sim_clients, requests_per_client=20, n_opt=7,
+              seed=0x2011011106 + rank, device=local, delta_micro=args.delta_micro or 100_000)
+    with ClockSampler(local) as clk:
+        pol = {p: pkg.simulate(pkg.SimConfig(policy=p, **kw)) for p in ("planner", "edf", "lcf", "rr")}
+    p = pol["planner"]
+    t = torch.tensor([p["sim_seconds"], p["gpu_seconds"]], dtype=torch.float64,
+                     device=torch.device("cuda", local))
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        sec = float(t[0])
+        print(json.dumps({
+            "metric": "simulated requests/sec (RTDeepIoT planner, closed-loop edge servers)",
+            "value": p["requests"] * world / sec, "unit": "requests/s", "n_gpus": world, "steps": 1,
+            "warmup": 0, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded request traces)",
+            "config": {"workload": f"sim {servers} servers x {args.sim_clients} clients x 20 requests, 8 stages",
+                       "delta_micro": kw["delta_micro"]},
+            "plans_per_s": p["plans"] * world / sec, "gpu_fraction": float(t[1]) / sec,
+            "policies": {k: {"accuracy": v["accuracy"], "miss_rate": v["miss_rate"],
+                             "mean_depth": v["mean_depth"]} for k, v in pol.items()},
+            "clocks": clk.summary(),
+        }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -340,9 +373,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--op", default="solve", choices=["solve", "reassign", "replan"],
+    ap.add_argument("--sim-clients", type=int, default=12, help="--op simulate: clients per server")
+    ap.add_argument("--op", default="solve", choices=["solve", "reassign", "replan", "simulate"],
                     help="reassign: the stage-completion update (NEXT-3, Eq. 5) on the solved batch; replan: "
-                         "one arrival per instance re-planned from its row (NEXT-2, needs --delta-micro)")
+                         "one arrival per instance re-planned from its row (NEXT-2, needs --delta-micro); simulate: "
+                         "the edge-server simulator, planner vs EDF/LCF/RR (NEXT-4)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -390,6 +425,11 @@ def main():
         id0 = weak_shard(n_inst, rank)[0]
         hash_id0 = id0
         spans = [(id0, id0 + n_inst)]
+    if args.op == "simulate":
+        run_simulate(args, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     stream = torch.cuda.Stream(dev)
 
     # ---- inputs resident in HBM: this rank's global-id shard, generated on device

@@ -1,0 +1,61 @@
+/* ic_sim.h — NEXT-4: event-driven simulation of RTDeepIoT edge servers (§III-B,
+ * §IV) on synthetic traces, many independent servers advanced in
+ * lockstep so the planner's DP runs as one GPU batch across servers.
+ *
+ * Model (integer ticks; confidence in micro-units):
+ *   - each server runs one stage at a time, non-preemptively;
+ *   - K closed-loop clients per server; a client issues its next request `think` ticks
+ *     after the previous one is answered; relative deadline D ~ U{d_lo..d_hi}
+ *     (P:L245-246); adjusted deadline = arrival + D - max stage WCET;
+ *   - a request is an anytime network of 1 + n_opt stages, WCET w_j = wcet_base *
+ *     (1 + U[0,10%)) (the 99%-CI bound stand-in), true confidence after stage j
+ *     from the generator's easy/hard mixture with residual shrink rho (gen/ic_gen_core.h);
+ *   - outcome: the confidence of the last stage completed by the raw deadline;
+ *     none completed = a deadline miss (counted with confidence 0).
+ * Policies:
+ *   IC_SIM_PLANNER — RTDeepIoT: at every scheduling point after an arrival or a stage
+ *     completion the server's pending requests are re-planned with the paper's
+ *     DP (ic_sched_solve_batch_host, Delta = delta_micro; completed stages are sunk,
+ *     SPEC S:L237), then the EDF-first request with planned stages left runs its next stage.
+ *     Utility: IC_SIM_UTIL_EXP (prior r_0 before the first stage, then Exp) or
+ *     IC_SIM_UTIL_ORACLE (the true curve, RTDeepIoT-OPT).
+ *   IC_SIM_EDF — full depth, earliest deadline first;  IC_SIM_LCF — least current
+ *   confidence first (unstarted lowest, ties earlier deadline);  IC_SIM_RR — stage-level
+ *   round robin in arrival order.
+ * Returns 0 on success, -1 invalid config, -3 CUDA error (planner only: the baselines
+ * need no GPU).  Deterministic for a given config. */
+#ifndef IC_SIM_H
+#define IC_SIM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { IC_SIM_PLANNER = 0, IC_SIM_EDF = 1, IC_SIM_LCF = 2, IC_SIM_RR = 3 };
+enum { IC_SIM_UTIL_EXP = 0, IC_SIM_UTIL_ORACLE = 1 };
+
+typedef struct {
+  int32_t servers, clients, requests_per_client, n_opt;
+  int32_t wcet_base, d_lo, d_hi, think;
+  uint64_t seed;
+  int32_t policy, utility;
+  uint32_t delta_micro;  /* planner's Delta (paper default 0.1 = 100000) */
+  uint32_t prior_micro;  /* planner's confidence prior before a request's first stage */
+  int32_t device;
+} ic_sim_config;
+
+typedef struct {
+  int64_t requests, misses, stages_run, plans, rounds;
+  int64_t conf_micro;     /* sum of the outcome confidences */
+  double accuracy;        /* conf_micro / 1e6 / requests (misses count 0) */
+  double miss_rate, mean_depth;
+  double sim_seconds, gpu_seconds;
+} ic_sim_result;
+
+int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

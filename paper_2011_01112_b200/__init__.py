@@ -21,4 +21,6 @@ from .abi import (  # noqa: F401
     INPUT_FIELDS, OUTPUT_FIELDS, STATS_FIELDS,
     SchedConfig, SchedInfo, Scheduler, ICSchedError, lib_path, load_library,
     alloc_inputs, alloc_outputs, gen_batch_device,
+    IC_SIM_PLANNER, IC_SIM_EDF, IC_SIM_LCF, IC_SIM_RR, IC_SIM_UTIL_EXP, IC_SIM_UTIL_ORACLE,
+    SimConfig, SimResult, simulate,
 )

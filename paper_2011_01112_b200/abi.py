@@ -76,7 +76,7 @@ class _GenCfg(ctypes.Structure):
 
 EXPORTED = ("ic_sched_create", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
             "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch", "ic_sched_state_bytes",
-            "ic_sched_solve_batch_state", "ic_sched_replan_batch")
+            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sim_run")
 
 IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
 
@@ -84,6 +84,49 @@ IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
 class _Upd(ctypes.Structure):
     _fields_ = [("kept", ctypes.c_void_p), ("done", ctypes.c_void_p), ("observed", ctypes.c_void_p),
                 ("heuristic", ctypes.c_int32)]
+
+IC_SIM_PLANNER, IC_SIM_EDF, IC_SIM_LCF, IC_SIM_RR = 0, 1, 2, 3
+IC_SIM_UTIL_EXP, IC_SIM_UTIL_ORACLE = 0, 1
+SIM_POLICIES = {"planner": IC_SIM_PLANNER, "edf": IC_SIM_EDF, "lcf": IC_SIM_LCF, "rr": IC_SIM_RR}
+
+
+class SimConfig(ctypes.Structure):
+    """include/ic_sim.h ic_sim_config."""
+    _fields_ = [("servers", ctypes.c_int32), ("clients", ctypes.c_int32),
+                ("requests_per_client", ctypes.c_int32), ("n_opt", ctypes.c_int32),
+                ("wcet_base", ctypes.c_int32), ("d_lo", ctypes.c_int32), ("d_hi", ctypes.c_int32),
+                ("think", ctypes.c_int32), ("seed", ctypes.c_uint64), ("policy", ctypes.c_int32),
+                ("utility", ctypes.c_int32), ("delta_micro", ctypes.c_uint32), ("prior_micro", ctypes.c_uint32),
+                ("device", ctypes.c_int32)]
+
+    def __init__(self, servers=1, clients=20, requests_per_client=50, n_opt=7, wcet_base=10, d_lo=10,
+                 d_hi=300, think=1, seed=0x2011011106, policy=IC_SIM_PLANNER, utility=IC_SIM_UTIL_EXP,
+                 delta_micro=100_000, prior_micro=500_000, device=0):
+        if isinstance(policy, str):
+            policy = SIM_POLICIES[policy]
+        super().__init__(servers, clients, requests_per_client, n_opt, wcet_base, d_lo, d_hi, think, seed,
+                         policy, utility, delta_micro, prior_micro, device)
+
+
+class SimResult(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("requests", "misses", "stages_run", "plans", "rounds",
+                                              "conf_micro")] + \
+               [(n, ctypes.c_double) for n in ("accuracy", "miss_rate", "mean_depth", "sim_seconds",
+                                               "gpu_seconds")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+def simulate(cfg: SimConfig) -> dict:
+    """ic_sim_run: event-driven edge-server simulation (include/ic_sim.h, NEXT-4)."""
+    lib = load_library()
+    r = SimResult()
+    rc = lib.ic_sim_run(ctypes.byref(cfg), ctypes.byref(r))
+    if rc != 0:
+        raise ICSchedError("ic_sim_run", rc)
+    return r.as_dict()
+
 
 _lib = None
 
@@ -114,6 +157,7 @@ def load_library():
                                                    ctypes.c_void_p]
         lib.ic_sched_replan_batch.argtypes = [ctypes.c_void_p, P(_In), ctypes.c_void_p, P(_Out), ctypes.c_void_p]
         lib.ic_sched_state_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        lib.ic_sim_run.argtypes = [P(SimConfig), P(SimResult)]
         for f in EXPORTED:
             getattr(lib, f).restype = ctypes.c_int
         lib.ic_sched_state_bytes.restype = ctypes.c_int64
