@@ -337,7 +337,7 @@ def run_simulate(args, rank, world, local):
     import torch.distributed as dist
     import paper_2011_01112_b200 as pkg
     servers = args.instances or 2048
-    kw = dict(servers=servers, clients=args.sim_clients, requests_per_client=20, n_opt=7,
+    kw = dict(servers=servers, clients=args.sim_clients, requests_per_client=20, n_opt=7, period=args.sim_period,
               seed=0x2011011106 + rank, device=local, delta_micro=args.delta_micro or 100_000)
     with ClockSampler(local) as clk:
         pol = {p: pkg.simulate(pkg.SimConfig(policy=p, **kw)) for p in ("planner", "edf", "lcf", "rr")}
@@ -349,11 +349,12 @@ def run_simulate(args, rank, world, local):
     if rank == 0:
         sec = float(t[0])
         print(json.dumps({
-            "metric": "simulated requests/sec (RTDeepIoT planner, closed-loop edge servers)",
+            "metric": "simulated requests/sec (RTDeepIoT planner, edge-server simulation)",
             "value": p["requests"] * world / sec, "unit": "requests/s", "n_gpus": world, "steps": 1,
             "warmup": 0, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded request traces)",
-            "config": {"workload": f"sim {servers} servers x {args.sim_clients} clients x 20 requests, 8 stages",
+            "config": {"workload": f"sim {servers} servers x {args.sim_clients} clients x 20 requests, 8 stages, "
+                                   + (f"open loop period {args.sim_period}" if args.sim_period else "closed loop"),
                        "delta_micro": kw["delta_micro"]},
             "plans_per_s": p["plans"] * world / sec, "gpu_fraction": float(t[1]) / sec,
             "policies": {k: {"accuracy": v["accuracy"], "miss_rate": v["miss_rate"],
@@ -373,7 +374,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sim-clients", type=int, default=12, help="--op simulate: clients per server")
+    ap.add_argument("--sim-clients", type=int, default=20, help="--op simulate: clients per server")
+    ap.add_argument("--sim-period", type=int, default=600, help="--op simulate: open-loop mean gap (0: closed loop)")
     ap.add_argument("--op", default="solve", choices=["solve", "reassign", "replan", "simulate"],
                     help="reassign: the stage-completion update (NEXT-3, Eq. 5) on the solved batch; replan: "
                          "one arrival per instance re-planned from its row (NEXT-2, needs --delta-micro); simulate: "

@@ -4,9 +4,13 @@
  *
  * Model (integer ticks; confidence in micro-units):
  *   - each server runs one stage at a time, non-preemptively;
- *   - K closed-loop clients per server; a client issues its next request `think` ticks
- *     after the previous one is answered; relative deadline D ~ U{d_lo..d_hi}
- *     (P:L245-246); adjusted deadline = arrival + D - max stage WCET;
+ *   - K clients per server.  period == 0: closed loop, a client issues its next request
+ *     `think` ticks after the previous one is answered; period > 0: open loop, gaps between
+ *     a client's requests uniform in [period/2, 3*period/2] ("within a time
+ *     interval"; S:L357 for the closed loop); relative deadline D ~ U{d_lo..d_hi}
+ *     (P:L245-246).  The planner plans only at GPU-idle instants, where no running stage
+ *     can block the plan, so it uses the raw deadline (the P:L73-75 one-stage adjustment
+ *     covers a scheduler invoked while a stage runs; reading R22);
  *   - a request is an anytime network of 1 + n_opt stages, WCET w_j = wcet_base *
  *     (1 + U[0,10%)) (the 99%-CI bound stand-in), true confidence after stage j
  *     from the generator's easy/hard mixture with residual shrink rho (gen/ic_gen_core.h);
@@ -16,7 +20,7 @@
  *   IC_SIM_PLANNER — RTDeepIoT: at every scheduling point after an arrival or a stage
  *     completion the server's pending requests are re-planned with the paper's
  *     DP (ic_sched_solve_batch_host, Delta = delta_micro; completed stages are sunk,
- *     SPEC S:L237), then the EDF-first request with planned stages left runs its next stage.
+ *     SPEC S:L237, and each task is valued floor(conf/Delta) - floor(current/Delta)), then the EDF-first request with planned stages left runs its next stage.
  *     Utility: IC_SIM_UTIL_EXP (prior r_0 before the first stage, then Exp) or
  *     IC_SIM_UTIL_ORACLE (the true curve, RTDeepIoT-OPT).
  *   IC_SIM_EDF — full depth, earliest deadline first;  IC_SIM_LCF — least current
@@ -43,6 +47,7 @@ typedef struct {
   uint32_t delta_micro;  /* planner's Delta (paper default 0.1 = 100000) */
   uint32_t prior_micro;  /* planner's confidence prior before a request's first stage */
   int32_t device;
+  int32_t period;        /* 0: closed loop (think); > 0: open loop, mean gap in ticks */
 } ic_sim_config;
 
 typedef struct {

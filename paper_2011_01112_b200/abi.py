@@ -97,15 +97,15 @@ class SimConfig(ctypes.Structure):
                 ("wcet_base", ctypes.c_int32), ("d_lo", ctypes.c_int32), ("d_hi", ctypes.c_int32),
                 ("think", ctypes.c_int32), ("seed", ctypes.c_uint64), ("policy", ctypes.c_int32),
                 ("utility", ctypes.c_int32), ("delta_micro", ctypes.c_uint32), ("prior_micro", ctypes.c_uint32),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("period", ctypes.c_int32)]
 
     def __init__(self, servers=1, clients=20, requests_per_client=50, n_opt=7, wcet_base=10, d_lo=10,
                  d_hi=300, think=1, seed=0x2011011106, policy=IC_SIM_PLANNER, utility=IC_SIM_UTIL_EXP,
-                 delta_micro=100_000, prior_micro=500_000, device=0):
+                 delta_micro=100_000, prior_micro=500_000, device=0, period=0):
         if isinstance(policy, str):
             policy = SIM_POLICIES[policy]
         super().__init__(servers, clients, requests_per_client, n_opt, wcet_base, d_lo, d_hi, think, seed,
-                         policy, utility, delta_micro, prior_micro, device)
+                         policy, utility, delta_micro, prior_micro, device, period)
 
 
 class SimResult(ctypes.Structure):

@@ -20,7 +20,7 @@ constexpr int64_t NEVER = INT64_MAX / 4;
 constexpr int KMAX = 15;
 
 struct Req {
-  int64_t arrive, dabs, dadj;
+  int64_t arrive, dabs;
   int client, s, planned;
   int64_t best;  // outcome so far: confidence of the last stage done by dabs
   int32_t w[KMAX], R[KMAX];
@@ -60,13 +60,12 @@ Req make_request(const Sim& S, int server, int client, int seq, int64_t t) {
   const int easy = (int)(x[1] >> 31);
   const int64_t a0 = easy ? ic_gen_uniform(x[2], 800000, 990000) : ic_gen_uniform(x[2], 100000, 600000);
   const uint32_t rho = (uint32_t)ic_gen_uniform(x[3], 19661, 52429);
-  int64_t wmax = 0, resid = 1000000 - a0;
+  int64_t resid = 1000000 - a0;
   for (int j = 0; j < S.L; ++j) {
     if ((j & 3) == 0) ic_gen_draw(c.seed, gid, 1u, 1u + (uint32_t)(j >> 2), y);
     const uint64_t f = (uint64_t)ic_gen_mulhi32(y[j & 3], 6554u);
     const int64_t w = std::max<int64_t>(1, ((int64_t)c.wcet_base * (65536 + (int64_t)f) + 32768) >> 16);
     q.w[j] = (int32_t)w;
-    wmax = std::max(wmax, w);
     if (j == 0) {
       q.R[0] = (int32_t)a0;
     } else {
@@ -75,9 +74,18 @@ Req make_request(const Sim& S, int server, int client, int seq, int64_t t) {
       resid = nr;
     }
   }
+  // The planner runs only at GPU-idle instants, so no stage can block the plan it makes:
+  // the raw deadline is exact there and the P:L73-75 one-stage adjustment is not needed.
   q.dabs = t + D;
-  q.dadj = q.dabs - wmax;  // one stage of non-preemption subtracted
   return q;
+}
+
+// Open loop: the gap to a client's next request, uniform in [period/2, 3*period/2].
+int64_t open_gap(const Sim& S, int server, int client, int seq) {
+  uint32_t x[4];
+  ic_gen_draw(S.c.seed, ((uint64_t)server << 32) | ((uint64_t)client << 20) | (uint64_t)seq, 3u, 0u, x);
+  const int64_t p = S.c.period;
+  return std::max<int64_t>(1, ic_gen_uniform(x[0], p / 2, p + p / 2));
 }
 
 void answer(Sim& S, Server& v, int idx, int64_t t) {
@@ -86,9 +94,7 @@ void answer(Sim& S, Server& v, int idx, int64_t t) {
   S.conf += q.best;
   if (q.best == 0) S.misses++;
   const int c = q.client;
-  if (v.client_left[c] > 0) {
-    v.client_next[c] = t + S.c.think;
-  }
+  if (S.c.period == 0 && v.client_left[c] > 0) v.client_next[c] = t + S.c.think;  // closed loop
   if (v.running > idx) v.running--;
   if (v.rr_last >= idx) v.rr_last--;
   v.reqs.erase(v.reqs.begin() + idx);
@@ -99,12 +105,15 @@ void answer(Sim& S, Server& v, int idx, int64_t t) {
 bool advance(Sim& S, Server& v) {
   const int pol = S.c.policy;
   for (;;) {
+    // Answer requests past their deadline, with every stage done, or — started ones —
+    // done with their planned stages.  An unstarted request the plan dropped stays pending
+    // until its deadline: later re-plans may admit it.
+    for (int i = (int)v.reqs.size() - 1; i >= 0; --i) {
+      if (i == v.running) continue;
+      const Req& q = v.reqs[i];
+      if (q.s >= S.L || q.dabs <= v.now || (q.s > 0 && q.s >= q.planned)) answer(S, v, i, v.now);
+    }
     if (v.running < 0) {
-      // answer requests that are finished or past their deadline
-      for (int i = (int)v.reqs.size() - 1; i >= 0; --i) {
-        const Req& q = v.reqs[i];
-        if (q.s >= q.planned || q.s >= S.L || q.dabs <= v.now) answer(S, v, i, v.now);
-      }
       if (!v.reqs.empty()) {
         if (pol == IC_SIM_PLANNER && v.dirty) return true;
         int pick = -1;
@@ -116,11 +125,11 @@ bool advance(Sim& S, Server& v) {
           bool better;
           if (pol == IC_SIM_LCF) {
             const int64_t cq = q.s ? q.R[q.s - 1] : -1, cp = p.s ? p.R[p.s - 1] : -1;
-            better = cq < cp || (cq == cp && (q.dadj < p.dadj || (q.dadj == p.dadj && q.arrive < p.arrive)));
+            better = cq < cp || (cq == cp && (q.dabs < p.dabs || (q.dabs == p.dabs && q.arrive < p.arrive)));
           } else if (pol == IC_SIM_RR) {
             better = false;  // handled below
           } else {
-            better = q.dadj < p.dadj || (q.dadj == p.dadj && q.arrive < p.arrive);
+            better = q.dabs < p.dabs || (q.dabs == p.dabs && q.arrive < p.arrive);
           }
           if (better) pick = i;
         }
@@ -140,10 +149,13 @@ bool advance(Sim& S, Server& v) {
         }
       }
     }
-    // next event: an arrival or the completion of the stage in flight (arrivals first)
+    // next event: an arrival, the completion of the stage in flight, or a waiting request's
+    // deadline (arrivals first, then the completion, at equal times)
     int64_t t_arr = NEVER;
     for (size_t c = 0; c < v.client_next.size(); ++c)
       if (v.client_left[c] > 0) t_arr = std::min(t_arr, v.client_next[c]);
+    for (int i = 0; i < (int)v.reqs.size(); ++i)
+      if (i != v.running) t_arr = std::min(t_arr, v.reqs[i].dabs);
     const int64_t t_done = v.running >= 0 ? v.busy_until : NEVER;
     const int64_t t = std::min(t_arr, t_done);
     if (t >= NEVER) {
@@ -155,7 +167,7 @@ bool advance(Sim& S, Server& v) {
       if (v.client_left[c] > 0 && v.client_next[c] == t) {
         v.reqs.push_back(make_request(S, (int)(&v - &S.sv[0]), (int)c, v.client_seq[c]++, t));
         v.client_left[c]--;
-        v.client_next[c] = NEVER;
+        v.client_next[c] = S.c.period ? t + open_gap(S, (int)(&v - &S.sv[0]), (int)c, v.client_seq[c]) : NEVER;
         v.dirty = true;
       }
     }
@@ -186,12 +198,17 @@ void build_instance(const Sim& S, const Server& v, std::vector<int64_t>& tb, std
         pred[j] = j == 0 ? S.c.prior_micro : prev + (1000000 - prev) / 2;  // Exp
       }
     }
+    // Completed stages are sunk: the DP values each task relative to its current
+    // confidence `base`.  Carrying base mod Delta into the mandatory value makes the DP's
+    // floor(R/Delta) equal floor(pred/Delta) - floor(base/Delta), i.e. the paper's objective
+    // (quantised total confidence, Eq. 1) minus a per-plan constant.
     const int64_t base = q.s ? q.R[q.s - 1] : 0;
+    const int64_t carry = base % (int64_t)S.c.delta_micro;
     rel.push_back(0);
-    dl.push_back((int32_t)std::max<int64_t>(-1, std::min<int64_t>(q.dadj - v.now, (int64_t)INT32_MAX / 2)));
+    dl.push_back((int32_t)std::max<int64_t>(-1, std::min<int64_t>(q.dabs - v.now, (int64_t)INT32_MAX / 2)));
     mw.push_back(q.w[q.s]);
     no.push_back((uint8_t)(S.L - 1 - q.s));
-    mc.push_back((uint32_t)std::max<int64_t>(0, pred[q.s] - base));
+    mc.push_back((uint32_t)std::max<int64_t>(0, pred[q.s] - base + carry));
     for (int k = 0; k < st; ++k) {
       const int j = q.s + 1 + k;
       ow.push_back(j < S.L ? q.w[j] : 0);
@@ -207,7 +224,7 @@ extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) {
   if (!cfg || !out) return -1;
   const ic_sim_config c = *cfg;
   if (c.servers < 1 || c.clients < 1 || c.requests_per_client < 1 || c.n_opt < 0 || c.n_opt > KMAX - 1 ||
-      c.wcet_base < 1 || c.d_lo < 1 || c.d_hi < c.d_lo || c.think < 1 || c.policy < 0 || c.policy > 3 ||
+      c.wcet_base < 1 || c.d_lo < 1 || c.d_hi < c.d_lo || c.think < 1 || c.period < 0 || c.policy < 0 || c.policy > 3 ||
       (c.policy == IC_SIM_PLANNER && c.delta_micro == 0))
     return -1;
   const auto t0 = std::chrono::steady_clock::now();
@@ -230,7 +247,12 @@ extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) {
   double gpu_s = 0;
   if (c.policy == IC_SIM_PLANNER) {
     // horizon: every adjusted deadline relative to a scheduling point is < d_hi
-    ic_sched_config sc{c.device, IC_DROP_ALLOWED, c.delta_micro, 0, c.clients, c.n_opt, c.d_hi + 1};
+    // pending requests: one per client (closed loop), or every arrival within the last
+    // d_hi ticks (open loop, gaps >= period/2)
+    const int64_t per = c.period ? (int64_t)c.clients * ((int64_t)c.d_hi / std::max(1, c.period / 2) + 1)
+                                 : (int64_t)c.clients;
+    ic_sched_config sc{c.device, IC_DROP_ALLOWED, c.delta_micro, 0, (int32_t)std::min<int64_t>(per, 4096),
+                       c.n_opt, c.d_hi + 1};
     const int rc = ic_sched_create(&sc, &h);
     if (rc != IC_OK) return rc == IC_ERR_CUDA ? -3 : -1;
   }
