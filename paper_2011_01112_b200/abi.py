@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "libicsched.so")
+_LIB = os.environ.get("IC_SCHED_LIB") or os.path.join(_HERE, "libicsched.so")  # override: A/B builds only
 
 IC_OK, IC_ERR_INVALID_ARG, IC_ERR_LIMIT, IC_ERR_CUDA, IC_ERR_OOM = 0, -1, -2, -3, -4
 IC_DROP_ALLOWED, IC_MANDATORY_ENFORCED = 0, 1

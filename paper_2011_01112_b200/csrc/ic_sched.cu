@@ -156,16 +156,29 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
     if (dec_smem) ndec = 1;
   }
   if (env && !strcmp(env, "global1")) ndec = 1;
-  const Layout L = make_layout(c, nw, sb, pad, dec_smem, nslots, ndec);
+  Layout L = make_layout(c, nw, sb, pad, dec_smem, nslots, ndec);
 
   KernelFn fn = kernel_for(nw, sb, drop);
   if (!fn) return IC_ERR_LIMIT;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes) != cudaSuccess)
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) != cudaSuccess)
     return IC_ERR_CUDA;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (nw + 1), L.bytes) != cudaSuccess)
     return IC_ERR_CUDA;
   if (per_sm < 1) return IC_ERR_LIMIT;
+  // Spend the shared memory the occupancy leaves over on a wider pad: rows whose options
+  // reach past it take the (slower) edge path for their first chunk.
+  if (!getenv("IC_SCHED_PAD")) {
+    for (int p2 = pad + 32; p2 <= c.max_horizon; p2 += 32) {
+      const Layout L2 = make_layout(c, nw, sb, p2, dec_smem, nslots, ndec);
+      int o2 = 0;
+      if (L2.bytes > kSmemLimit ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fn, 32 * (nw + 1), L2.bytes) != cudaSuccess ||
+          o2 < per_sm)
+        break;
+      L = L2;
+    }
+  }
   per_sm = env_int("IC_SCHED_CTAS", per_sm) < per_sm ? env_int("IC_SCHED_CTAS", per_sm) : per_sm;
 
   ic_sched* h = (ic_sched*)calloc(1, sizeof(ic_sched));
