@@ -63,7 +63,6 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
   L.ndec = ndec;
   L.off_rowp = o;   o = align16(o + (ns * mt * L.kp + 8) * 8);
   L.off_info = o;   o = align16(o + ns * mt * 16);
-  L.off_tR = o;     o = align16(o + ns * mt * L.r1 * 4);
   L.off_task = o;   o = align16(o + ns * mt * 4);
   L.off_tail = o;   o = align16(o + ns * mt * 4);
   L.off_misc = o;   o = align16(o + 3 * 16 * 8);
@@ -340,7 +339,6 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.off_dec = L.off_dec;
   p.off_rowp = L.off_rowp;
   p.off_info = L.off_info;
-  p.off_tR = L.off_tR;
   p.off_task = L.off_task;
   p.off_tail = L.off_tail;
   p.off_misc = L.off_misc;

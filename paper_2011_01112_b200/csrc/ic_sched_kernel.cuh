@@ -290,7 +290,6 @@ struct Smem {
   uint32_t* dec;
   int2* rowp;    // [2][max_tasks][kp]  (C_k, key_k) of EDF row pos
   int4* info;    // [2][max_tasks]      (d, K | gen<<8 | S<<16, r, d_next)
-  int32_t* tR;   // [2][max_tasks][r1]  cumulative confidence of EDF row pos
   int32_t* task; // [2][max_tasks]      input index of EDF row pos
   int32_t* tail; // [2][max_tasks]      tail nibble of row pos
   long long* misc;  // [2][16]
@@ -435,14 +434,12 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       d = S.sd[tk];
       const int r = S.sr[tk], Sn = S.sS[tk];
       int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
-      int32_t* trp = S.tR + ((size_t)s * p.max_tasks + pos) * p.r1;
       long long C = p.mand_wcet[t], R = p.mand_conf[t];
       auto option = [&](int k) {
         const int q = (int)(R / delta);
         qmax = max(qmax, q);
         if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
           rp[k] = make_int2((int)C, (q << 4) - (k + 1));
-          trp[k] = (int)R;
           K = k + 1;
         }
       };
@@ -588,7 +585,12 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
       a = Cc;
       bb = (long long)r + Cc;
       Q += (o.y + code) >> 4;
-      conf += S.tR[((size_t)s * p.max_tasks + pos) * p.r1 + code - 1];
+      {  // R_i(code-1), re-read from the (L2-resident) descriptors
+        const int64_t t = lo + tk;
+        long long R = p.mand_conf[t];
+        for (int j = 0; j < code - 1; ++j) R += p.opt_gain[t * p.smax + j];
+        conf += R;
+      }
       nopt += code - 1;
     } else if (valid) {
       ndrop += 1;
@@ -657,7 +659,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
   S.dec = p.dec_smem ? (uint32_t*)(smem + p.off_dec) : p.dec_global + (int64_t)blockIdx.x * p.dec_slab_words;
   S.rowp = (int2*)(smem + p.off_rowp);
   S.info = (int4*)(smem + p.off_info);
-  S.tR = (int32_t*)(smem + p.off_tR);
   S.task = (int32_t*)(smem + p.off_task);
   S.tail = (int32_t*)(smem + p.off_tail);
   S.misc = (long long*)(smem + p.off_misc);
