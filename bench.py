@@ -529,6 +529,28 @@ def main():
     total_inst = cw.n_instances if strong else n_inst * world
     value = total_inst * args.steps / (ms / 1e3)
 
+    # ---- C1-sized batches are launch-bound: per-solve latency by CUDA-graph replay
+    # (SURVEY.md §8(d)); the graph holds one ic_sched_solve_batch launch on `stream`
+    latency = None
+    if n_inst <= 64:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            sched.solve_batch(inputs, out, stream)  # warm the launch path outside capture
+            stream.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                sched.solve_batch(inputs, out, stream)
+            for _ in range(20):
+                g.replay()
+            reps = 2000
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            e1.record(stream)
+        e1.synchronize()
+        latency = {"graph_replay_us": e0.elapsed_time(e1) * 1e3 / reps, "launch_us": kern_ms * 1e3,
+                   "instances_per_solve": n_inst}
+
     # ---- end to end through the public host-buffer entry point (pinned H2D + solve + D2H)
     e2e = None
     if not args.no_e2e:
@@ -592,6 +614,8 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if latency:
+            line["latency"] = latency
         if world == 1 and not args.no_cpu_baseline:
             v, n, el, thr = cpu_oracle_rate(cw, args, args.cpu_seconds)
             line["cpu_baseline"] = {"value": v, "unit": "instances/s", "cores": thr, "kind": "oracle",

@@ -36,11 +36,11 @@ struct Layout {
   int bytes, nq, kp, r1, np2, pad, rs, nbuf;
   int off_rowbuf, off_dec, off_rowp, off_info, off_tR, off_task, off_tail, off_misc, off_chosen, off_sd, off_sr,
       off_sS, off_key, off_aux, off_sQ;
-  int nslots, ndec, cap;
+  int nslots, ndec, cap, rowp_global;
 };
 
 Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_smem, int nslots = 2,
-                   int ndec = 1) {
+                   int ndec = 1, int rowp_global = 0) {
   Layout L{};
   const int nt = 32 * nw;
   const int cols = (c.max_horizon + nt - 1) / nt;
@@ -61,7 +61,8 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
   L.off_rowbuf = o; o = align16(o + L.nbuf * L.rs * 4);
   L.off_dec = o;    if (dec_smem) o = align16(o + ndec * mt * L.nq * nt * 4);
   L.ndec = ndec;
-  L.off_rowp = o;   o = align16(o + (ns * mt * L.kp + 8) * 8);
+  L.rowp_global = rowp_global;  // option tables of both slots in global memory, one copy in smem
+  L.off_rowp = o;   o = align16(o + ((rowp_global ? 1 : ns) * mt * L.kp + 8) * 8);
   L.off_info = o;   o = align16(o + ns * mt * 16);
   L.off_task = o;   o = align16(o + ns * mt * 4);
   L.off_tail = o;   o = align16(o + ns * mt * 4);
@@ -89,6 +90,8 @@ struct ic_sched {
   int dec_smem, sms, ctas_per_sm, grid;
   uint32_t* dec_global;
   int64_t dec_slab_words;
+  int2* rowp_g;
+  int64_t rowp_slab;
   unsigned long long* work;
   void* stage;
   size_t stage_bytes;
@@ -139,8 +142,17 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
     Lg = make_layout(c, nw, true, pad, false);
   }
   int nslots = env_int("IC_SCHED_SLOTS", 2) == 1 ? 1 : 2;
+  // large task sets: keep both slots' option tables in a global (L2) slab so the setup
+  // and backtrack still overlap the sweep (IC_SCHED_ROWP=global forces it for tests)
+  const char* rowp_env = getenv("IC_SCHED_ROWP");
+  int rowp_global = rowp_env && !strcmp(rowp_env, "global") ? 1 : 0;
+  if (nslots == 2 && nw >= 8 && (Lg.bytes > kSmemLimit || rowp_global)) {  // compiled for NW >= 8 only
+    rowp_global = 1;
+    Lg = make_layout(c, nw, sb, pad, false, 2, 1, 1);
+  }
   if (Lg.bytes > kSmemLimit || nslots == 1) {  // serialise setup and sweep to fit large task sets
     nslots = 1;
+    rowp_global = 0;
     Lg = make_layout(c, nw, sb, pad, false, 1);
   }
   if (Lg.bytes > kSmemLimit) return IC_ERR_LIMIT;
@@ -150,12 +162,12 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   bool dec_smem = false;
   const char* env = getenv("IC_SCHED_DEC");
   if (env && !strcmp(env, "smem")) {
-    Layout Ls = make_layout(c, nw, sb, pad, true, nslots, 1);
+    Layout Ls = make_layout(c, nw, sb, pad, true, nslots, 1, rowp_global);
     dec_smem = Ls.bytes <= kSmemLimit;
     if (dec_smem) ndec = 1;
   }
   if (env && !strcmp(env, "global1")) ndec = 1;
-  Layout L = make_layout(c, nw, sb, pad, dec_smem, nslots, ndec);
+  Layout L = make_layout(c, nw, sb, pad, dec_smem, nslots, ndec, rowp_global);
 
   KernelFn fn = kernel_for(nw, sb, drop);
   if (!fn) return IC_ERR_LIMIT;
@@ -169,7 +181,7 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   // reach past it take the (slower) edge path for their first chunk.
   if (!getenv("IC_SCHED_PAD")) {
     for (int p2 = pad + 32; p2 <= c.max_horizon; p2 += 32) {
-      const Layout L2 = make_layout(c, nw, sb, p2, dec_smem, nslots, ndec);
+      const Layout L2 = make_layout(c, nw, sb, p2, dec_smem, nslots, ndec, rowp_global);
       int o2 = 0;
       if (L2.bytes > kSmemLimit ||
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, fn, 32 * (nw + 1), L2.bytes) != cudaSuccess ||
@@ -198,6 +210,16 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   if (!dec_smem) {
     h->dec_slab_words = (int64_t)c.max_tasks * L.nq * 32 * nw * L.ndec;
     if (cudaMalloc(&h->dec_global, (size_t)h->dec_slab_words * 4 * h->grid) != cudaSuccess) {
+      cudaFree(h->work);
+      free(h);
+      return IC_ERR_OOM;
+    }
+  }
+  if (L.rowp_global) {
+    h->rowp_slab = (int64_t)2 * c.max_tasks * L.kp + 8;
+    if (cudaMalloc(&h->rowp_g, (size_t)h->rowp_slab * 8 * h->grid) != cudaSuccess) {
+      if (h->dec_global) cudaFree(h->dec_global);
+      cudaFree(h->work);
       free(h);
       return IC_ERR_OOM;
     }
@@ -210,6 +232,7 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
   if (!h) return IC_ERR_INVALID_ARG;
   cudaSetDevice(h->cfg.device);
   if (h->dec_global) cudaFree(h->dec_global);
+  if (h->rowp_g) cudaFree(h->rowp_g);
   if (h->work) cudaFree(h->work);
   if (h->stage) cudaFree(h->stage);
   if (h->s_in) {
@@ -233,7 +256,7 @@ extern "C" int ic_sched_get_info(const ic_sched* h, ic_sched_info* info) {
   info->decisions_in_smem = h->dec_smem;
   info->double_buffered = h->sb ? 0 : 1;
   info->pad_cols = h->L.pad;
-  info->workspace_bytes = h->dec_smem ? 0 : h->dec_slab_words * 4 * h->grid;
+  info->workspace_bytes = (h->dec_smem ? 0 : h->dec_slab_words * 4 * h->grid) + h->rowp_slab * 8 * h->grid;
   return IC_OK;
 }
 
@@ -362,6 +385,10 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.work = h->work;
   p.ndec = L.ndec;
   p.dec_words = (int64_t)h->cfg.max_tasks * L.nq * 32 * h->nw;
+  p.rowp_g = h->rowp_g;
+  p.rowp_slab = h->rowp_slab;
+  p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
+               ((uintptr_t)p.opt_gain & 15) == 0 && !getenv("IC_SCHED_NOVEC");
   int64_t grid = h->grid;
   if (grid > in->n_instances) grid = in->n_instances;
   h->fn<<<(unsigned)grid, 32 * (h->nw + 1), h->L.bytes, (cudaStream_t)cuda_stream>>>(p);

@@ -32,6 +32,10 @@
 
 #include <type_traits>
 
+#ifndef IC_PRED_CHUNK
+#define IC_PRED_CHUNK 0
+#endif
+
 namespace icsched {
 
 constexpr int NEG = -(1 << 30);
@@ -78,6 +82,11 @@ struct Params {
   int ckpt;    // rows kept in the state: every ckpt-th (rows ckpt-1, 2 ckpt-1, ...), power of two
   unsigned long long* work;  // [2] dynamic instance counter, CTAs finished (reset by the last CTA)
   int rowbuf_stride;  // ints per row buffer (pad + capacity)
+  // large task sets: the tail warp's option tables of both slots live in a per-CTA global
+  // (L2) slab and the DP warps copy the current one into their single shared-memory table
+  int2* rowp_g;
+  int64_t rowp_slab;  // int2 per CTA slab ([2][max_tasks][kp])
+  int opt_vec4;       // optional-stage rows are 16-byte aligned multiples of 4: LDG.128 loads
 };
 
 __device__ __forceinline__ int32_t* state_rows(const Params& p, int64_t b) {
@@ -176,6 +185,23 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     auto chunk = [&](int g0, auto clamp_tag) {
       const int tb = g0 * NT + tid;
       uint32_t dw = 0;
+#if IC_PRED_CHUNK
+      // one predicated 8-group body serves full and ragged chunks (half the code per K)
+      const int rem = ng - g0;
+#pragma unroll
+      for (int h = 0; h < 8; h += BATCH) {
+        int v[BATCH];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) v[u] = (h + u < rem) ? cell(tb + (h + u) * NT, clamp_tag) : 0;
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          if (h + u < rem) {
+            dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
+            nxt[tb + (h + u) * NT] = stv(v[u]);
+          }
+        }
+      }
+#else
       if (g0 + 8 <= ng) {
 #pragma unroll
         for (int h = 0; h < 8; h += BATCH) {
@@ -208,6 +234,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         if (rem & 2) sub(std::integral_constant<int, 2>{});
         if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
+#endif
       decrow[(g0 >> 3) * NT + tid] = dw;
     };
     int g0 = 0;
@@ -289,6 +316,7 @@ struct Smem {
   int32_t* rowbuf;
   uint32_t* dec;
   int2* rowp;    // [2][max_tasks][kp]  (C_k, key_k) of EDF row pos
+                 //   ([1][...] when the tables live in global memory: the DP's copy)
   int4* info;    // [2][max_tasks]      (d, K | gen<<8 | S<<16, r, d_next)
   int32_t* task; // [2][max_tasks]      input index of EDF row pos
   int32_t* tail; // [2][max_tasks]      tail nibble of row pos
@@ -299,6 +327,20 @@ struct Smem {
   int32_t* sQ;   // [max_tasks]     staging: prefix of max quantised reward
   unsigned long long* key;
 };
+
+// Global option tables are compiled only into the wide kernels (NW >= 8: the large task
+// sets that need them), so the small kernels keep their register budget.
+template <int NW>
+__device__ __forceinline__ bool rowp_global(const Params& p) {
+  if constexpr (NW >= 8) return p.rowp_g != nullptr;
+  return false;
+}
+// The tail warp's option table of slot s: shared memory, or the CTA's global slab.
+template <int NW>
+__device__ __forceinline__ int2* rowp_slot(const Params& p, const Smem& S, int s) {
+  return rowp_global<NW>(p) ? p.rowp_g + (int64_t)blockIdx.x * p.rowp_slab + (int64_t)s * p.max_tasks * p.kp
+                            : S.rowp + (size_t)s * p.max_tasks * p.kp;
+}
 
 // Write the "everything dropped" outputs of an instance that the DP never sees.
 __device__ __forceinline__ void write_dropped(const Params& p, int64_t b, int64_t lo, int64_t n, int status,
@@ -318,16 +360,25 @@ __device__ __forceinline__ void write_dropped(const Params& p, int64_t b, int64_
 }
 
 // Visit task t's optional stages k = 1..Sn with (wcet, gain), loading them in
-// batches of 4 independent loads (the tail warp's register budget is small).
+// batches of 4 (the tail warp's register budget is small): one 128-bit load per
+// array and batch when the rows allow it (lane-per-task: a warp reads 32 whole
+// consecutive rows, so every sector fetched is used), else 4 scalar loads.
 template <typename F>
 __device__ __forceinline__ void for_each_opt(const Params& p, int64_t t, int Sn, F&& f) {
   for (int k0 = 0; k0 < Sn; k0 += 4) {
     int w[4], g[4];
+    if (p.opt_vec4) {  // k0 + 3 < smax: the load stays inside task t's row
+      const int4 w4 = *(const int4*)(p.opt_wcet + t * p.smax + k0);
+      const int4 g4 = *(const int4*)(p.opt_gain + t * p.smax + k0);
+      w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+      g[0] = g4.x; g[1] = g4.y; g[2] = g4.z; g[3] = g4.w;
+    } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (k0 + u < Sn) {
-        w[u] = p.opt_wcet[t * p.smax + k0 + u];
-        g[u] = p.opt_gain[t * p.smax + k0 + u];
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < Sn) {
+          w[u] = p.opt_wcet[t * p.smax + k0 + u];
+          g[u] = p.opt_gain[t * p.smax + k0 + u];
+        }
       }
     }
 #pragma unroll
@@ -433,7 +484,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       const int64_t t = lo + tk;
       d = S.sd[tk];
       const int r = S.sr[tk], Sn = S.sS[tk];
-      int2* rp = S.rowp + ((size_t)s * p.max_tasks + pos) * p.kp;
+      int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
       long long C = p.mand_wcet[t], R = p.mand_conf[t];
       auto option = [&](int k) {
         const int q = (int)(R / delta);
@@ -531,7 +582,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
     if (mi[5] >= 0) {
       int t = (int)mi[6];
       const int4* inf = S.info + s * p.max_tasks;
-      const int2* rp = S.rowp + (size_t)s * p.max_tasks * p.kp;
+      const int2* rp = rowp_slot<NW>(p, S, s);
       const bool rw = mi[9] != 0;
       for (int pos = n - 1; pos >= 0; --pos) {
         const int d = inf[pos].x;  // time axis: deadline; reward axis: last reachable column
@@ -559,6 +610,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
 }
 
 // a7/a8: EDF schedule (warp max-plus scan), outputs in input order, stats.
+template <int NW>
 __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int s, int lane,
                                              unsigned long long (&acc)[8]) {
   const long long* mi = S.misc + s * 16;
@@ -580,7 +632,7 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
     }
     long long a = 0, bb = -(1LL << 62);  // map x -> max(x + a, bb)
     if (code > 0) {
-      const int2 o = S.rowp[((size_t)s * p.max_tasks + pos) * p.kp + code - 1];
+      const int2 o = rowp_slot<NW>(p, S, s)[(size_t)pos * p.kp + code - 1];
       Cc = o.x;
       a = Cc;
       bb = (long long)r + Cc;
@@ -686,6 +738,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     int64_t b = claim();
     while (b < p.B && tail_setup<NW>(p, S, b, 0, lane, acc) != ST_OK) b = claim();
     if (b >= p.B && lane == 0) S.misc[3] = ST_END;
+    if (rowp_global<NW>(p)) __threadfence_block();  // the global option table is visible to the DP warps
     __syncwarp();
     bar_arrive(BAR_READY, NT + 32);
     if (p.nslots == 2) {
@@ -696,6 +749,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         int64_t nb = claim();
         while (nb < p.B && tail_setup<NW>(p, S, nb, s ^ 1, lane, acc) != ST_OK) nb = claim();
         if (nb >= p.B && lane == 0) S.misc[(s ^ 1) * 16 + 3] = ST_END;
+        if (rowp_global<NW>(p)) __threadfence_block();
         __syncwarp();
         bar_sync(BAR_DONE, NT + 32);  // the DP warps finished instance b
         if (p.ndec == 2) {
@@ -705,7 +759,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
           tail_backtrack<NW>(p, S, s, lane, db);
           bar_arrive(BAR_READY, NT + 32);  // decisions free: the DP warps may start nb
         }
-        tail_outputs(p, S, s, lane, acc);
+        tail_outputs<NW>(p, S, s, lane, acc);
         b = nb;
         ++it;
       }
@@ -713,10 +767,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       while (b < p.B) {
         bar_sync(BAR_DONE, NT + 32);
         tail_backtrack<NW>(p, S, 0, lane, 0);
-        tail_outputs(p, S, 0, lane, acc);
+        tail_outputs<NW>(p, S, 0, lane, acc);
         int64_t nb = claim();
         while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb = claim();
         if (nb >= p.B && lane == 0) S.misc[3] = ST_END;
+        if (rowp_global<NW>(p)) __threadfence_block();
         __syncwarp();
         bar_arrive(BAR_READY, NT + 32);
         b = nb;
@@ -762,6 +817,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       for (int bb = 0; bb < (SB ? 1 : 2); ++bb)
         for (int i = tid; i < p.pad; i += NT) S.rowbuf[bb * RS + i] = rw ? INFV : NEG;
     }
+    if (rowp_global<NW>(p)) {  // this instance's option table: global (L2) slab -> shared memory
+      const int4* src = (const int4*)rowp_slot<NW>(p, S, s);
+      int4* dst = (int4*)S.rowp;
+      for (int i = tid; i < n * p.kp / 2; i += NT) dst[i] = src[i];
+    }
     if (rw) {  // P(0, 0) = 0, P(0, r > 0) = infinity
       for (int t = tid; t <= d_first; t += NT) buf0[t] = t == 0 ? 0 : INFV;
       if (tid == 0) *rmax_slot = -1;
@@ -770,7 +830,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     }
     bar_sync(BAR_DP, NT);
     const int4* inf = S.info + s * p.max_tasks;
-    const int2* rpb = S.rowp + (size_t)s * p.max_tasks * p.kp;
+    const int2* rpb = rowp_global<NW>(p) ? S.rowp : S.rowp + (size_t)s * p.max_tasks * p.kp;
     const int32_t* auxp = S.aux + s * p.max_tasks;
     int M = 15;
     const size_t dec_row_words = (size_t)p.nq * NT;

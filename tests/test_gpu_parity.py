@@ -214,7 +214,10 @@ def test_full_size_sampled(name, sample):
                                  {"IC_SCHED_NW": "16"}, {"IC_SCHED_SB": "1", "IC_SCHED_NW": "8"},
                                  {"IC_SCHED_SB": "1", "IC_SCHED_NW": "16", "IC_SCHED_DEC": "global"},
                                  {"IC_SCHED_PAD": "32"}, {"IC_SCHED_SLOTS": "1", "IC_SCHED_NW": "2"},
-                                 {"IC_SCHED_SLOTS": "1", "IC_SCHED_SB": "1", "IC_SCHED_NW": "8"}])
+                                 {"IC_SCHED_SLOTS": "1", "IC_SCHED_SB": "1", "IC_SCHED_NW": "8"},
+                                 {"IC_SCHED_ROWP": "global", "IC_SCHED_NW": "8"},
+                                 {"IC_SCHED_ROWP": "global", "IC_SCHED_SB": "1", "IC_SCHED_NW": "16"},
+                                 {"IC_SCHED_ROWP": "global", "IC_SCHED_NW": "8", "IC_SCHED_DEC": "global1"}])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_every_kernel_variant(monkeypatch, env, mode):
     """Every compiled (DP warps, in-place rows, drop mode, decision placement) variant agrees."""
