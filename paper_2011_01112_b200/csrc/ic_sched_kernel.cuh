@@ -32,8 +32,11 @@
 
 #include <type_traits>
 
-#ifndef IC_PRED_CHUNK
-#define IC_PRED_CHUNK 0
+#ifndef IC_BATCH_KSPLIT
+#define IC_BATCH_KSPLIT 6
+#endif
+#ifndef IC_BATCH_HI
+#define IC_BATCH_HI 4
 #endif
 
 namespace icsched {
@@ -181,27 +184,10 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   // stored value: time axis keeps low nibble 15 (the drop key), reward axis keeps it 0
   auto stv = [](int v) { return RW ? (v & ~15) : (v | 15); };
   if (!SB) {
-    constexpr int BATCH = (KK <= 6) ? 8 : 4;  // cells whose loads are in flight together
+    constexpr int BATCH = (KK <= IC_BATCH_KSPLIT) ? 8 : IC_BATCH_HI;  // cells whose loads are in flight together
     auto chunk = [&](int g0, auto clamp_tag) {
       const int tb = g0 * NT + tid;
       uint32_t dw = 0;
-#if IC_PRED_CHUNK
-      // one predicated 8-group body serves full and ragged chunks (half the code per K)
-      const int rem = ng - g0;
-#pragma unroll
-      for (int h = 0; h < 8; h += BATCH) {
-        int v[BATCH];
-#pragma unroll
-        for (int u = 0; u < BATCH; ++u) v[u] = (h + u < rem) ? cell(tb + (h + u) * NT, clamp_tag) : 0;
-#pragma unroll
-        for (int u = 0; u < BATCH; ++u) {
-          if (h + u < rem) {
-            dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
-            nxt[tb + (h + u) * NT] = stv(v[u]);
-          }
-        }
-      }
-#else
       if (g0 + 8 <= ng) {
 #pragma unroll
         for (int h = 0; h < 8; h += BATCH) {
@@ -234,7 +220,6 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         if (rem & 2) sub(std::integral_constant<int, 2>{});
         if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
-#endif
       decrow[(g0 >> 3) * NT + tid] = dw;
     };
     int g0 = 0;
