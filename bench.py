@@ -227,7 +227,7 @@ def run_reference(args, cw, rank, world):
     v = n * args.steps / el
     line = {"metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": "strong" if cw.u_blocks and not args.instances else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "impl": "reference", "config": workload_config(cw, args, n),
             "cpu_baseline": {"value": v, "unit": "instances/s", "cores": threads, "kind": "oracle",
                              "sample": f"{n} instances of {cw.name} per step, paper reward-indexed DP (O2)"},

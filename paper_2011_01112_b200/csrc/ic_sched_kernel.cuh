@@ -684,7 +684,10 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
 
 // ---------------------------------------------------------------------------
 // Resident CTAs per SM the register budget is sized for (85/113/102/113/120 registers).
-constexpr int min_blocks(int nw) { return nw == 1 ? 12 : nw == 2 ? 6 : nw == 4 ? 4 : nw == 8 ? 2 : 1; }
+#ifndef IC_MINB1
+#define IC_MINB1 12
+#endif
+constexpr int min_blocks(int nw) { return nw == 1 ? IC_MINB1 : nw == 2 ? 6 : nw == 4 ? 4 : nw == 8 ? 2 : 1; }
 
 template <int NW, bool SB, bool DROP>
 __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(const Params p) {
