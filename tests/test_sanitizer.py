@@ -1,0 +1,31 @@
+"""compute-sanitizer over every kernel family (SURVEY.md §4.2 / §5 race detection).
+
+memcheck (out-of-bounds and misaligned accesses), racecheck (shared-memory hazards
+between the warp-specialised tail and DP warps, which hand buffers over through
+named barriers) and synccheck (barrier misuse) on small solves of each variant in
+tests/sanitize_driver.py; only the library's kernels are instrumented.
+"""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "3", "--kernel-name", "kns=ic_dp_kernel",
+           sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    tail = (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0, f"{tool} exit {r.returncode}:\n{tail}"
+    # memcheck/synccheck print "ERROR SUMMARY: 0 errors", racecheck "RACECHECK SUMMARY: 0 hazards ..."
+    assert re.search(r"ERROR SUMMARY: 0 errors|RACECHECK SUMMARY: 0 hazards displayed \(0 errors, 0 warnings\)",
+                     r.stdout + r.stderr), tail
+    assert r.stdout.count("ok ") >= 5, tail
