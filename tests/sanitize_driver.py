@@ -28,11 +28,67 @@ VARIANTS = {
     "reward_axis": ({"IC_SCHED_AXIS": "2"}, "C2", 6, 100_000),
 }
 KNOBS = ("IC_SCHED_SB", "IC_SCHED_NW", "IC_SCHED_ROWP", "IC_SCHED_AXIS")
+EXTRA = ("replan", "reassign")
+
+
+def _first_tasks(batch, m):
+    from gen import Batch
+    parts = []
+    for b in range(batch.n_instances):
+        one = batch.instance(b)
+        parts.append(Batch(np.array([0, m], np.int64), one.release[:m], one.deadline[:m], one.mand_wcet[:m],
+                           one.n_opt[:m], one.opt_wcet[:m], one.mand_conf[:m], one.opt_gain[:m]))
+    return gen.concat(parts, batch.opt_stride)
+
+
+def replan():
+    """NEXT-2 state path: solve 31 tasks keeping the state, re-plan with one arrival."""
+    import torch
+    import paper_2011_01112_b200 as pkg
+    from tests.gpu_util import to_device
+    cw = gen.WorkloadConfig("C2x", 0, 32, 4, 1024, 0.6, 1.0, 35, 0x2011011102)
+    full = gen.generate(cw, 6)
+    sc = pkg.SchedConfig(max_tasks=32, max_opt_stages=4, max_horizon=1024, delta_micro=100_000)
+    with pkg.Scheduler(sc) as s:
+        state = torch.zeros(s.state_bytes(full.n_instances), dtype=torch.uint8, device="cuda")
+        s.solve_batch_state(to_device(_first_tasks(full, 31)), state)
+        out = s.replan_batch(to_device(full), state)
+        torch.cuda.synchronize()
+        got = {k: v.cpu().numpy() for k, v in out.items()}
+    ref = oracle.solve(full, oracle.OracleConfig(delta_micro=100_000, max_tasks=32, max_horizon=1024), oracle.TIME)
+    assert_parity(got, ref, "sanitize replan")
+
+
+def reassign():
+    """NEXT-3 stage-completion kernel on a solved C2-shaped batch."""
+    import torch
+    import paper_2011_01112_b200 as pkg
+    from tests.gpu_util import to_device
+    cw = gen.CONFIGS["C2"]
+    batch = gen.generate(cw, 16)
+    ocfg = oracle.OracleConfig(delta_micro=100_000, max_tasks=32, max_horizon=1024)
+    plan = oracle.solve(batch, ocfg, oracle.TIME)
+    done = np.zeros(batch.n_instances, np.int8)
+    obs = np.full(batch.n_instances, 300_000, np.uint32)
+    ref = oracle.reassign(batch, plan["kept"], done, obs, 2, ocfg)
+    sc = pkg.SchedConfig(max_tasks=32, max_opt_stages=4, max_horizon=1024, delta_micro=100_000)
+    with pkg.Scheduler(sc) as s:
+        out = s.reassign_batch(to_device(batch), torch.from_numpy(plan["kept"]).cuda(),
+                               torch.from_numpy(done).cuda(), torch.from_numpy(obs).cuda(), 2)
+        torch.cuda.synchronize()
+    for k in ("kept", "start", "finish", "conf_micro", "makespan", "status", "swapped"):
+        np.testing.assert_array_equal(out[k].cpu().numpy(), ref[k], err_msg=k)
 
 
 def main(names):
     rng = np.random.default_rng(7)
     for name in names:
+        for k in KNOBS:
+            os.environ.pop(k, None)
+        if name in EXTRA:
+            {"replan": replan, "reassign": reassign}[name]()
+            print("ok", name, flush=True)
+            continue
         env, cfg, n, delta = VARIANTS[name]
         for k in KNOBS:
             os.environ.pop(k, None)
@@ -51,4 +107,4 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or list(VARIANTS))
+    main(sys.argv[1:] or list(VARIANTS) + list(EXTRA))

@@ -3,7 +3,8 @@
 memcheck (out-of-bounds and misaligned accesses), racecheck (shared-memory hazards
 between the warp-specialised tail and DP warps, which hand buffers over through
 named barriers) and synccheck (barrier misuse) on small solves of each variant in
-tests/sanitize_driver.py; only the library's kernels are instrumented.
+tests/sanitize_driver.py, plus the NEXT-2 state/re-plan path and the NEXT-3
+reassignment kernel; only the library's kernels are instrumented.
 """
 import os
 import re
@@ -21,6 +22,7 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer(tool):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "3", "--kernel-name", "kns=ic_dp_kernel",
+           "--kernel-name", "kns=reassign_kernel",
            sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     tail = (r.stdout + r.stderr)[-4000:]
@@ -28,4 +30,4 @@ def test_compute_sanitizer(tool):
     # memcheck/synccheck print "ERROR SUMMARY: 0 errors", racecheck "RACECHECK SUMMARY: 0 hazards ..."
     assert re.search(r"ERROR SUMMARY: 0 errors|RACECHECK SUMMARY: 0 hazards displayed \(0 errors, 0 warnings\)",
                      r.stdout + r.stderr), tail
-    assert r.stdout.count("ok ") >= 5, tail
+    assert r.stdout.count("ok ") >= 7, tail
