@@ -32,6 +32,9 @@
 
 #include <type_traits>
 
+#ifndef IC_SB_CHUNK
+#define IC_SB_CHUNK 8
+#endif
 #ifndef IC_BATCH_KSPLIT
 #define IC_BATCH_KSPLIT 6
 #endif
@@ -230,28 +233,32 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
     // chunk c reads only columns below its top, so writing it after the barrier
     // cannot disturb a lower chunk still to be computed.
-    const int nch = d >= 0 ? (d / NT) / 8 + 1 : 0;  // CTA-uniform chunk count (warp 0 has the most groups)
+    constexpr int CH = IC_SB_CHUNK;  // groups per chunk (a multiple of 8: one decision word per 8)
+    const int nch = d >= 0 ? (d / NT) / CH + 1 : 0;  // CTA-uniform chunk count (warp 0 has the most groups)
     for (int c = nch - 1; c >= 0; --c) {
-      const int g0 = c * 8;
+      const int g0 = c * CH;
       const int tb = g0 * NT + tid;
-      int v[8];
+      int v[CH];
       if (gcl > 0 && g0 < gcl) {  // rare: options longer than the pad
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::true_type{}) : 0;
+        for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::true_type{}) : 0;
       } else {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::false_type{}) : 0;
+        for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::false_type{}) : 0;
       }
       bar_sync(BAR_DP, NT);
-      uint32_t dw = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (g0 + u < ng) {
-          dw |= (uint32_t)(v[u] & 15) << (4 * u);
-          nxt[tb + u * NT] = stv(v[u]);
+      for (int w8 = 0; w8 < CH; w8 += 8) {
+        uint32_t dw = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (g0 + w8 + u < ng) {
+            dw |= (uint32_t)(v[w8 + u] & 15) << (4 * u);
+            nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
+          }
         }
+        if (g0 + w8 < ng) decrow[((g0 + w8) >> 3) * NT + tid] = dw;
       }
-      if (g0 < ng) decrow[(g0 >> 3) * NT + tid] = dw;
     }
   }
 }
