@@ -142,14 +142,9 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     }
   }
   int reachC = 0;
-  if (RW) {  // (C, (q<<4)-(k+1)) -> shift q, add C*16 + k+1
+  if (RW) {  // the tail warp stored the reward-axis form: shift q, add C*16 + k+1
 #pragma unroll
-    for (int k = 0; k < KK; ++k) {
-      const int q = (key[k] + k + 1) >> 4;
-      key[k] = min(C[k], 1 << 20) * 16 + (k + 1);
-      C[k] = q;
-      reachC = max(reachC, q);
-    }
+    for (int k = 0; k < KK; ++k) reachC = max(reachC, C[k]);
   } else if (KK > 0) {
     reachC = C[KK - 1];
   }
@@ -307,7 +302,7 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
 struct Smem {
   int32_t* rowbuf;
   uint32_t* dec;
-  int2* rowp;    // [2][max_tasks][kp]  (C_k, key_k) of EDF row pos
+  int2* rowp;    // [2][max_tasks][kp]  (C_k, key_k) of EDF row pos; reward axis: (q_k, C_k*16 + k+1)
                  //   ([1][...] when the tables live in global memory: the DP's copy)
   int4* info;    // [2][max_tasks]      (d, K | gen<<8 | S<<16, r, d_next)
   int32_t* task; // [2][max_tasks]      input index of EDF row pos
@@ -534,6 +529,14 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       int4* f = S.info + s * p.max_tasks + pos;
       f->x = S.sQ[pos];
       f->w = pos + 1 < n ? S.sQ[pos + 1] : INT32_MIN;
+      // option table in the reward-axis form, once per row here rather than per row and
+      // thread in the sweep: (C, (q << 4) - (k+1)) -> (q, C*16 + k+1)
+      int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
+      const int K = f->y & 255;
+      for (int k = 0; k < K; ++k) {
+        const int2 o = rp[k];
+        rp[k] = make_int2((o.y + k + 1) >> 4, min(o.x, 1 << 20) * 16 + (k + 1));
+      }
     }
   }
   __syncwarp();
@@ -589,7 +592,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
         }
         if (rw) {  // reward axis: the nibble is the code; step to column r - q
           S.chosen[pos] = nib;
-          if (nib > 0) t -= (rp[(size_t)pos * p.kp + nib - 1].y + nib) >> 4;
+          if (nib > 0) t -= rp[(size_t)pos * p.kp + nib - 1].x;  // (q, C*16 + code)
         } else {
           const int code = 15 - nib;
           S.chosen[pos] = code;
@@ -609,6 +612,7 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
   const int n = (int)mi[0];
   const int64_t lo = mi[1], b = mi[2];
   const bool feasible = mi[5] >= 0;
+  const bool rw = mi[9] != 0;  // option table in the reward-axis form (q, C*16 + code)
   const int4* inf = S.info + s * p.max_tasks;
   long long F = 0, Q = 0, conf = 0, ndrop = 0, nopt = 0, noff = 0;
   for (int base = 0; base < n; base += 32) {
@@ -625,10 +629,10 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
     long long a = 0, bb = -(1LL << 62);  // map x -> max(x + a, bb)
     if (code > 0) {
       const int2 o = rowp_slot<NW>(p, S, s)[(size_t)pos * p.kp + code - 1];
-      Cc = o.x;
+      Cc = rw ? (o.y - code) >> 4 : o.x;
       a = Cc;
       bb = (long long)r + Cc;
-      Q += (o.y + code) >> 4;
+      Q += rw ? o.x : (o.y + code) >> 4;
       {  // R_i(code-1), re-read from the (L2-resident) descriptors
         const int64_t t = lo + tk;
         long long R = p.mand_conf[t];
