@@ -823,7 +823,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       for (int i = tid; i < n * p.kp / 2; i += NT) dst[i] = src[i];
     }
     if (rw) {  // P(0, 0) = 0, P(0, r > 0) = infinity
-      for (int t = tid; t <= d_first; t += NT) buf0[t] = t == 0 ? 0 : INFV;
+      // both row buffers start at infinity over every column the instance reaches
+      // (Qpre_N): Qpre is non-decreasing, so a row's unreachable columns
+      // (Qpre_pos, Qpre_next] were never written and need no per-row fill
+      const int qn = (int)mi[8];
+      for (int bb = 0; bb < (SB ? 1 : 2); ++bb)
+        for (int t = tid; t <= qn; t += NT) buf0[bb * RSb + t] = (t == 0 && bb == 0) ? 0 : INFV;
       if (tid == 0) *rmax_slot = -1;
     } else {
       for (int t = tid; t <= d_first; t += NT) buf0[t] = 15;  // G_0(t) = 0
@@ -861,11 +866,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         // reward axis: columns r <= Qpre_pos; (Qpre_pos, Qpre_next] are unreachable
         dp_row_dispatch<NW, SB, DROP, true>(K, false, cur, nxt, decrow, (const int4*)ops, d, 0, p.pad,
                                             auxp[pos]);
-        if (dn > d) {
-          const int first = d + 1;
-#pragma unroll 1
-          for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = INFV;
-        }
         if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
           int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
           for (int t = tid; t <= d; t += NT) srow[t] = nxt[t];
