@@ -573,32 +573,49 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
   constexpr int NT = 32 * NW;
   const long long* mi = S.misc + s * 16;
   const int n = (int)mi[0];
-  if (lane == 0) {
-    if (mi[5] >= 0) {
-      int t = (int)mi[6];
-      const int4* inf = S.info + s * p.max_tasks;
-      const int2* rp = rowp_slot<NW>(p, S, s);
-      const bool rw = mi[9] != 0;
-      for (int pos = n - 1; pos >= 0; --pos) {
-        const int d = inf[pos].x;  // time axis: deadline; reward axis: last reachable column
-        int nib;
-        if (!rw && t > d) {
-          nib = S.tail[s * p.max_tasks + pos];
-        } else {
-          const int g = t / NT, l = t - g * NT;
-          const uint32_t* dbase = p.state ? state_dec(p, mi[2]) : S.dec + db * p.dec_words;
-          const uint32_t w = dbase[((size_t)pos * p.nq + (g >> 3)) * NT + l];
-          nib = (int)((w >> (4 * (g & 7))) & 15u);
-        }
-        if (rw) {  // reward axis: the nibble is the code; step to column r - q
-          S.chosen[pos] = nib;
-          if (nib > 0) t -= rp[(size_t)pos * p.kp + nib - 1].x;  // (q, C*16 + code)
-        } else {
-          const int code = 15 - nib;
-          S.chosen[pos] = code;
-          if (code > 0) t = min(t, d) - rp[(size_t)pos * p.kp + code - 1].x;
-        }
+  if (mi[5] >= 0) {
+    // Two rows per decision-word latency: while lane 31 fetches row pos's nibble at t,
+    // lanes 0..K_pos fetch row pos-1's nibble at every column its code could lead to
+    // (lane c: code c, 0 = drop); the true one is picked by a shuffle once row pos is
+    // decoded.  The chain of dependent (L2/HBM) loads halves; the result is unchanged.
+    int t = (int)mi[6];
+    const int4* inf = S.info + s * p.max_tasks;
+    const int2* rp = rowp_slot<NW>(p, S, s);
+    const bool rw = mi[9] != 0;
+    const uint32_t* dbase = p.state ? state_dec(p, mi[2]) : S.dec + db * p.dec_words;
+    const int32_t* tailn = S.tail + s * p.max_tasks;
+    // column the decision of code c at row `pos` (column t) leads to in row pos-1
+    auto step = [&](int pos, int tt, int code) -> int {
+      if (code == 0) return tt;
+      const int sh = rp[(size_t)pos * p.kp + code - 1].x;  // time axis: C; reward axis: q
+      return rw ? tt - sh : min(tt, inf[pos].x) - sh;
+    };
+    auto nibble = [&](int row, int tt) -> int {
+      if (!rw && tt > inf[row].x) return tailn[row];  // past the deadline: the row's tail nibble
+      const int g = tt / NT, l = tt - g * NT;
+      const uint32_t w = dbase[((size_t)row * p.nq + (g >> 3)) * NT + l];
+      return (int)((w >> (4 * (g & 7))) & 15u);
+    };
+    int pos = n - 1;
+    while (pos >= 0) {
+      const int K = inf[pos].y & 255;
+      int nib = 0;
+      if (lane == 31) {
+        nib = nibble(pos, t);
+      } else if (lane <= K && pos >= 1) {
+        const int tt = step(pos, t, lane);
+        if (tt >= 0) nib = nibble(pos - 1, tt);
       }
+      const int nib0 = __shfl_sync(0xffffffffu, nib, 31);
+      const int code0 = rw ? nib0 : 15 - nib0;
+      const int t1 = step(pos, t, code0);
+      if (lane == 0) S.chosen[pos] = code0;
+      if (pos == 0) break;
+      const int nib1 = __shfl_sync(0xffffffffu, nib, code0);
+      const int code1 = rw ? nib1 : 15 - nib1;
+      t = step(pos - 1, t1, code1);
+      if (lane == 0) S.chosen[pos - 1] = code1;
+      pos -= 2;
     }
   }
   __syncwarp();
