@@ -596,6 +596,20 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
       const uint32_t w = dbase[((size_t)row * p.nq + (g >> 3)) * NT + l];
       return (int)((w >> (4 * (g & 7))) & 15u);
     };
+    if (rowp_global<NW>(p)) {
+      // option tables in global memory: a speculative step would add a dependent global
+      // read per candidate, so the backtrack stays serial (C4: 5 % faster this way)
+      if (lane == 0) {
+        for (int pos = n - 1; pos >= 0; --pos) {
+          const int nb = nibble(pos, t);
+          const int code = rw ? nb : 15 - nb;
+          S.chosen[pos] = code;
+          t = step(pos, t, code);
+        }
+      }
+      __syncwarp();
+      return;
+    }
     int pos = n - 1;
     while (pos >= 0) {
       const int K = inf[pos].y & 255;
