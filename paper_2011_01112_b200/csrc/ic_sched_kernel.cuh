@@ -440,6 +440,28 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     unsigned long long x = lane < n ? S.key[lane] : ~0ull;
     x = warp_bitonic_sort(x, lane);
     if (lane < n) S.key[lane] = x;
+  } else if (np2 == 64) {  // two keys per lane (positions lane, lane + 32), in registers
+    unsigned long long x0 = S.key[lane], x1 = lane + 32 < n ? S.key[lane + 32] : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j == 32) {  // k = 64: partners lane and lane + 32, ascending
+          const unsigned long long lo2 = x0 < x1 ? x0 : x1;
+          x1 = x0 < x1 ? x1 : x0;
+          x0 = lo2;
+        } else {
+          const unsigned long long y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+          const unsigned long long y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+          const bool lower = (lane & j) == 0;
+          const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+          x0 = (lower == up0) ? (x0 < y0 ? x0 : y0) : (x0 < y0 ? y0 : x0);
+          x1 = (lower == up1) ? (x1 < y1 ? x1 : y1) : (x1 < y1 ? y1 : x1);
+        }
+      }
+    }
+    S.key[lane] = x0;
+    if (lane + 32 < n) S.key[lane + 32] = x1;
   } else {
     for (int i = n + lane; i < np2; i += 32) S.key[i] = ~0ull;
     __syncwarp();
