@@ -908,6 +908,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     int32_t* const tailp = S.tail + s * p.max_tasks;
     const int2* ops = rpb + (size_t)k0 * kp;
     uint32_t* decrow = decb + (size_t)k0 * dec_row_words;
+    const bool keep_state = p.state != nullptr;  // loop invariants, read once per instance
+    const int ckm = p.ckpt - 1;
 #pragma unroll 1
     for (int pos = k0; pos < n; ++pos) {
       const int4 fn = pos + 1 < n ? inf[pos + 1] : f;  // next row's header, off the critical path
@@ -919,7 +921,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         // reward axis: columns r <= Qpre_pos; (Qpre_pos, Qpre_next] are unreachable
         dp_row_dispatch<NW, SB, DROP, true>(K, false, cur, nxt, decrow, (const int4*)ops, d, 0, p.pad,
                                             auxp[pos]);
-        if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
+        if (keep_state && ((pos + 1) & ckm) == 0) {  // checkpoint row for later re-plans
           int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
           for (int t = tid; t <= d; t += NT) srow[t] = nxt[t];
         }
@@ -946,8 +948,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
           for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = Mn;
         }
         M = Mn;
-        if (p.state) {  // keep checkpoint rows for later re-plans: active columns, tail value
-          if (((pos + 1) & (p.ckpt - 1)) == 0) {
+        if (keep_state) {  // keep checkpoint rows for later re-plans: active columns, tail value
+          if (((pos + 1) & ckm) == 0) {
             int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
             for (int t = tid; t <= d; t += NT) srow[t] = nxt[t];
             if (tid == 0) srow[p.H] = Mn;
