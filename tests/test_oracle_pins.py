@@ -339,3 +339,84 @@ def test_checker_detects_violations():
     bad = {k: v.copy() for k, v in good.items()}
     bad["kept"][0] = -1
     assert oracle.check(b, bad, cfg)[0] != 0
+
+
+# ---------------------------------------------------------------- checker negative pins
+# Each bit of or_check (P:L48 schedule, P:L70 imprecise-computation feasibility, S:L494 EDF
+# demand criterion) is provoked by a hand-built result that breaks exactly that rule, beside a
+# near-miss at the boundary that must pass, so a dropped or inverted test fails here.
+def _res(kept, start, finish, q, conf, makespan, status=0):
+    return dict(kept=np.array(kept, np.int8), start=np.array(start, np.int32),
+                finish=np.array(finish, np.int32), q_total=np.array([q], np.int64),
+                conf_micro=np.array([conf], np.int64), makespan=np.array([makespan], np.int32),
+                status=np.array([status], np.uint8))
+
+
+CK = OracleConfig(delta_micro=100_000)
+CK_ENF = OracleConfig(drop_mode=1, delta_micro=100_000)
+
+
+def test_checker_bit1_start_before_release():
+    """a job cannot start before it is released (reading R9: start = max(F, r))."""
+    b = batch_from_tasks([dict(r=3, d=10, m=2, w=[], a0=500_000, g=[])])
+    assert oracle.check(b, _res([0], [3], [5], 5, 500_000, 5), CK)[0] == 0       # start == release
+    assert oracle.check(b, _res([0], [2], [4], 5, 500_000, 4), CK)[0] == 1       # one tick early
+
+
+def test_checker_bit4_finish_after_deadline():
+    """every kept task finishes by its (inclusive, adjusted) deadline."""
+    b = batch_from_tasks([dict(r=0, d=5, m=2, w=[], a0=500_000, g=[])])
+    assert oracle.check(b, _res([0], [3], [5], 5, 500_000, 5), CK)[0] == 0       # finish == deadline
+    assert oracle.check(b, _res([0], [4], [6], 5, 500_000, 6), CK)[0] == 4
+
+
+def test_checker_bit8_overlap():
+    """one GPU, jobs back to back in EDF order - a job may not start before the previous
+    kept job in that order has finished."""
+    ts = [dict(r=0, d=10, m=2, w=[], a0=500_000, g=[]), dict(r=0, d=10, m=2, w=[], a0=500_000, g=[])]
+    b = batch_from_tasks(ts)
+    assert oracle.check(b, _res([0, 0], [0, 2], [2, 4], 10, 1_000_000, 4), CK)[0] == 0   # touching
+    assert oracle.check(b, _res([0, 0], [0, 1], [2, 3], 10, 1_000_000, 3), CK)[0] == 8
+
+
+def test_checker_bit16_processor_demand():
+    """for all t1 < t2 the kept jobs released at or after t1 with deadline at most t2
+    need at most t2 - t1 ticks.  Two jobs of 3 ticks with a common deadline 5 cannot both be
+    kept (demand 6 > 5); at deadline 6 they can (demand == window)."""
+    ts = [dict(r=0, d=5, m=3, w=[], a0=500_000, g=[]), dict(r=0, d=5, m=3, w=[], a0=500_000, g=[])]
+    bits = oracle.check(batch_from_tasks(ts), _res([0, 0], [0, 3], [3, 6], 10, 1_000_000, 6), CK)[0]
+    assert bits & 16 and bits & 4
+    ok = [dict(t, d=6) for t in ts]
+    assert oracle.check(batch_from_tasks(ok), _res([0, 0], [0, 3], [3, 6], 10, 1_000_000, 6), CK)[0] == 0
+    # demand counted over the released window [t1, t2]: a late-released job only fits its own window
+    ts = [dict(r=4, d=6, m=3, w=[], a0=500_000, g=[]), dict(r=0, d=9, m=2, w=[], a0=500_000, g=[])]
+    bits = oracle.check(batch_from_tasks(ts), _res([0, 0], [4, 7], [7, 9], 10, 1_000_000, 9), CK)[0]
+    assert bits & 16          # job 0 alone: demand 3 in [4, 6]
+    ts[0]["d"] = 7
+    assert oracle.check(batch_from_tasks(ts), _res([0, 0], [4, 7], [7, 9], 10, 1_000_000, 9), CK)[0] == 0
+
+
+def test_checker_bit32_drop_when_enforced():
+    """P:L70 "if dropping entire tasks is disallowed": in ENFORCED mode a dropped task is a
+    violation; in DROP_ALLOWED mode the same plan is valid, and INFEASIBLE is never right there
+    (the empty plan is always feasible)."""
+    ts = [dict(r=0, d=10, m=2, w=[], a0=500_000, g=[]), dict(r=0, d=10, m=2, w=[], a0=300_000, g=[])]
+    b = batch_from_tasks(ts)
+    r = _res([0, -1], [0, -1], [2, -1], 5, 500_000, 2)
+    assert oracle.check(b, r, CK)[0] == 0
+    assert oracle.check(b, r, CK_ENF)[0] == 32
+    inf = _res([-1, -1], [-1, -1], [-1, -1], 0, 0, 0, status=oracle.INFEASIBLE)
+    assert oracle.check(b, inf, CK_ENF)[0] == 0
+    assert oracle.check(b, inf, CK)[0] == 32
+
+
+def test_checker_bits_64_128_bookkeeping():
+    """Q, confidence and makespan must be recomputable from the plan; kept out of [-1, S_i] or
+    a dropped task with times is an encoding error."""
+    b = batch_from_tasks([dict(r=0, d=10, m=2, w=[1], a0=500_000, g=[200_000])])
+    assert oracle.check(b, _res([1], [0], [3], 7, 700_000, 3), CK)[0] == 0
+    assert oracle.check(b, _res([1], [0], [3], 6, 700_000, 3), CK)[0] == 64       # Q
+    assert oracle.check(b, _res([1], [0], [3], 7, 699_999, 3), CK)[0] == 64       # confidence
+    assert oracle.check(b, _res([1], [0], [3], 7, 700_000, 4), CK)[0] == 64       # makespan
+    assert oracle.check(b, _res([2], [0], [3], 7, 700_000, 3), CK)[0] & 128       # kept > S_i
+    assert oracle.check(b, _res([-1], [0], [-1], 0, 0, 0), CK)[0] & 128           # drop with a start
