@@ -94,7 +94,7 @@ def algorithmic_evals(inputs, n_tasks, opt_stride, delta_micro=0, eps_micro=100_
             rmax = torch.where(feas, R, torch.zeros_like(R)).max(1).values.view(nb, N).max(1).values
             dl = torch.clamp(eps_micro * rmax // (1_000_000 * N), min=1)
         q = torch.where(valid, R // dl.repeat_interleave(N)[:, None], torch.zeros_like(R))
-        qmax = q.max(1).values.view(nb, N)
+        qmax = torch.where(fit, q, torch.zeros_like(q)).max(1).values.view(nb, N)  # options that fit
         key = d.view(nb, N) * (N + 1) + torch.arange(N, device=C.device)[None, :]  # EDF (d, idx); r = 0 here
         order = torch.argsort(key, 1)
         qpre = torch.cumsum(torch.gather(qmax, 1, order), 1)
@@ -176,61 +176,130 @@ def sample_batch(cw, n, salt=0):
     return gen.concat(parts, cw.n_opt)
 
 
-def _calibrate_oracle(cw, ocfg, threads, target_s):
-    """Instances of `cw` the oracle solves in about target_s seconds on `threads` threads."""
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_cfg(cw, delta_micro):
     import oracle
-    n = max(threads * 4, 32)
+    return oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=delta_micro, max_tasks=cw.n_tasks,
+                               max_horizon=cw.horizon)
+
+
+def _native_oracle():
+    """Load the oracle built -O3 -march=native for this host."""
+    import oracle
+    try:
+        oracle.use_native_build()
+        return "gcc -O3 -march=native"
+    except Exception:  # no compiler on the host: the portable -O3 build
+        return "gcc -O3"
+
+
+def _time_oracle(cw, ocfg, algo, threads, target_s, salt=0):
+    """Instances/s of the oracle (as it stands) on `threads` threads over a sample sized to run
+    about target_s seconds (calibrated on a smaller sample of other ids first)."""
+    import oracle
+    n = max(threads * 8, 32)
     while True:
-        sample = sample_batch(cw, n, salt=1 << 20)
+        cal = sample_batch(cw, n, salt=salt + (1 << 20))
         t0 = time.perf_counter()
-        oracle.solve(sample, ocfg, oracle.PAPER, threads)
+        oracle.solve(cal, ocfg, algo, threads)
         dt = time.perf_counter() - t0
-        if dt >= 1.0 or n >= cw.n_instances:
-            return int(min(cw.n_instances, max(threads, n * target_s / max(dt, 1e-6))))
+        if dt >= 0.5 or n >= cw.n_instances:
+            break
         n *= 4
+    rate = n / dt
+    for _ in range(3):  # the first calibration pass pays thread start-up and page faults
+        n = int(min(cw.n_instances, max(threads * 8, rate * target_s)))
+        sample = sample_batch(cw, n, salt=salt)
+        t0 = time.perf_counter()
+        oracle.solve(sample, ocfg, algo, threads)
+        el = time.perf_counter() - t0
+        rate = sample.n_instances / el
+        if el >= 0.6 * target_s or n >= cw.n_instances:
+            break
+    return rate, sample.n_instances, el
 
 
-def cpu_oracle_rate(cw, args, target_s):
-    """The oracle as it stands (paper DP, OpenMP over instances) on a bounded sample."""
+def cpu_oracle_baseline(cw, args, target_s):
+    """the oracle timed on the host cores, as it stands, built -O3 -march=native
+    for this host: O3 (the time-indexed DP, the scale oracle whose cost matches the GPU's) on
+    every core and on one core, plus O2 (the paper's reward-indexed DP, Eqs. 1-2) at the paper's
+    Delta = 0.1 beside it.  Bounded samples of the same workload."""
     import oracle
+    build = _native_oracle()
     threads = os.cpu_count() or 1
-    ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
-                               max_tasks=cw.n_tasks, max_horizon=cw.horizon)
-    n = _calibrate_oracle(cw, ocfg, threads, target_s)
-    sample = sample_batch(cw, n)
-    n = sample.n_instances
-    t0 = time.perf_counter()
-    oracle.solve(sample, ocfg, oracle.PAPER, threads)
-    el = time.perf_counter() - t0
-    return n / el, n, el, threads
+    v, n, el = _time_oracle(cw, _oracle_cfg(cw, args.delta_micro), oracle.TIME, threads, target_s)
+    v1, n1, el1 = _time_oracle(cw, _oracle_cfg(cw, args.delta_micro), oracle.TIME, 1, target_s / 4, salt=1 << 21)
+    v2, n2, el2 = _time_oracle(cw, _oracle_cfg(cw, 100_000), oracle.PAPER, threads, target_s / 4, salt=1 << 22)
+    part = "equal parts of every U block" if cw.u_blocks else "consecutive ids"
+    return {"value": v, "unit": "instances/s", "cores": threads, "kind": "oracle",
+            "sample": f"{n} {cw.name} instances ({part}), O3 time-indexed DP on {threads} OpenMP threads, {el:.1f} s",
+            "algorithm": "O3 (oracle/ic_oracle.c solve_time) at the workload's own Delta", "build": build,
+            "cpu_model": cpu_model(),
+            "single_thread": {"value": v1, "unit": "instances/s", "sample": f"{n1} instances, {el1:.1f} s"},
+            "paper_dp_delta_0_1": {"value": v2, "unit": "instances/s", "cores": threads,
+                                   "sample": f"{n2} instances, O2 (Eqs. 1-2, Alg. 1) at Delta = 0.1, {el2:.1f} s"}}
+
+
+# The paper's own figures for the method (context, not the target: different hardware, and the
+# paper's solver runs on the CPU with TensorFlow inference on the GPU, P:L206).  BASELINE.md §1.
+PAPER_CONTEXT = {
+    "hardware": "Intel i7-4770 (32 GB) + NVIDIA TITAN X Pascal, TensorFlow 1.14 (P:L251)",
+    "accuracy_gain_vs_edf_lcf_rr": "+10% ~ 20% (P:L6, P:L221)",
+    "deadline_misses": "(nearly) no deadline misses (P:L6)",
+    "exp_vs_opt_utility": "within 2% of optimal most of the time (P:L260-261, P:L273)",
+    "scheduler_overhead": "0.5% - 6% of per-request time, user-space CPU scheduler (P:L536, P:L541)",
+    "solver_throughput": "not reported (BASELINE.md §1)",
+}
+
+
+def smem_peak(local):
+    """Measured shared-memory load bandwidth of this GPU (include/ic_probe.h): the roofline
+    denominator of the sweep.  The larger of the LDS.32 and LDS.128 streams is the peak; the
+    LDS.32 + VIADDMNMX stream (the sweep's inner op) is reported beside it."""
+    import paper_2011_01112_b200 as pkg
+    r = {m: pkg.probe_smem(local, m, 60.0) for m in ("lds32", "lds128", "lds32_viaddmax")}
+    best = max(r.values(), key=lambda x: x["gbs"])
+    return {"gbs": best["gbs"], "bytes_per_clk_per_sm": best["bytes_per_clk_per_sm"], "mode": best["mode"],
+            "modes": {m: {"gbs": round(x["gbs"], 1), "bytes_per_clk_per_sm": round(x["bytes_per_clk_per_sm"], 2)}
+                      for m, x in r.items()}}
 
 
 def run_reference(args, cw, rank, world):
-    """--impl reference: the CPU oracle (paper DP) on the host cores, rank 0 only."""
+    """--impl reference: the CPU oracle (O3, -O3 -march=native) on the host cores, rank 0 only."""
     if rank != 0:
         return
     import oracle
+    build = _native_oracle()
     threads = os.cpu_count() or 1
-    ocfg = oracle.OracleConfig(epsilon_micro=cw.epsilon_micro, delta_micro=args.delta_micro,
-                               max_tasks=cw.n_tasks, max_horizon=cw.horizon)
+    ocfg = _oracle_cfg(cw, args.delta_micro)
     # size each step so the whole K+W-step run stays near two minutes of CPU work
     per_step = min(10.0, max(1.0, 120.0 / (args.steps + args.warmup)))
-    n = _calibrate_oracle(cw, ocfg, threads, per_step)
+    _, n, _ = _time_oracle(cw, ocfg, oracle.TIME, threads, per_step)
     sample = sample_batch(cw, n)
     n = sample.n_instances
     for _ in range(args.warmup):
-        oracle.solve(sample, ocfg, oracle.PAPER, threads)
+        oracle.solve(sample, ocfg, oracle.TIME, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.solve(sample, ocfg, oracle.PAPER, threads)
+        oracle.solve(sample, ocfg, oracle.TIME, threads)
     el = time.perf_counter() - t0
     v = n * args.steps / el
     line = {"metric": METRIC, "value": v, "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong" if cw.u_blocks and not args.instances else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "impl": "reference", "config": workload_config(cw, args, n),
+            "scaling": "strong" if cw.u_blocks and not args.instances else "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic", "impl": "reference", "config": workload_config(cw, args, n),
             "cpu_baseline": {"value": v, "unit": "instances/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{n} instances of {cw.name} per step, paper reward-indexed DP (O2)"},
+                             "sample": f"{n} instances of {cw.name} per step, O3 time-indexed DP ({build})",
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -381,6 +450,10 @@ def main():
                          "one arrival per instance re-planned from its row (NEXT-2, needs --delta-micro); simulate: "
                          "the edge-server simulator, planner vs EDF/LCF/RR (NEXT-4)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--lib", default=None, help="load libicsched from this path (A/B of two builds)")
+    ap.add_argument("--tune", action="append", default=[], metavar="FIELD=VALUE",
+                    help="ic_sched_tuning field for the handle (A/B of launch choices), repeatable")
+    ap.add_argument("--no-probe", action="store_true", help="skip the shared-memory peak probe")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -397,7 +470,10 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2011_01112_b200 as pkg
-    from paper_2011_01112_b200.multigpu import reduce_stats, shard_range, weak_shard
+    from paper_2011_01112_b200.multigpu import reduce_stats, shard_range, weak_shard, derived_metrics
+    if args.lib:
+        pkg.use_library(args.lib)
+    tuning = {k: int(v) for k, v in (t.split("=", 1) for t in args.tune)} or None
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -458,7 +534,7 @@ def main():
 
     sc = pkg.SchedConfig(device=local, max_tasks=cw.n_tasks, max_opt_stages=cw.n_opt, max_horizon=cw.horizon,
                          delta_micro=args.delta_micro, epsilon_micro=cw.epsilon_micro)
-    sched = pkg.Scheduler(sc)
+    sched = pkg.Scheduler(sc, tuning)
     info = sched.info()
     out = pkg.alloc_outputs(n_inst, T, device=dev)
     out_bytes = sum(v.numel() * v.element_size() for k, v in out.items() if k != "stats")
@@ -576,17 +652,23 @@ def main():
                "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(out_bytes + 64)}
 
     if rank == 0:
-        peaks = _peaks()
         sms = _sms()
         clk_s = clk.summary()
-        fmax = peaks.get("sm_max_mhz") or clk_s.get("sm_max_mhz") or 1965.0
-        peak_gbs = SMEM_BYTES_PER_CLK_PER_SM * sms * fmax * 1e6 / 1e9
+        fmax = _peaks().get("sm_max_mhz") or clk_s.get("sm_max_mhz") or 1965.0
+        nominal_gbs = SMEM_BYTES_PER_CLK_PER_SM * sms * fmax * 1e6 / 1e9
+        probe = None if args.no_probe else smem_peak(local)
+        peak_gbs = probe["gbs"] if probe else nominal_gbs
+        peak_basis = (f"measured: ic_probe_smem {probe['mode']} stream on {sms} SMs, "
+                      f"{probe['bytes_per_clk_per_sm']:.1f} B/clk/SM (include/ic_probe.h)") if probe else \
+            f"nominal 128 B/clk/SM x {sms} SMs x {fmax:.0f} MHz (probe skipped)"
         achieved = W * BYTES_PER_EVAL / (kern_ms / 1e3) / 1e9
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"ncu_{cw.name}_summary.json")
-        if os.path.exists(prof):
+        if os.path.exists(prof) and not args.delta_micro:
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_instance") * n_inst
+                ps = json.load(open(prof))
+                traffic = ps.get("dram_bytes_per_instance") * n_inst
+                traffic_src = f"{os.path.relpath(prof, ROOT)} ({ps.get('round', '?')}, {ps.get('kernel', '')})"
             except Exception:
                 traffic = None
         line = {
@@ -600,8 +682,9 @@ def main():
                            parallelism=f"instance shards x{world}"),
             "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                          "frac": achieved / peak_gbs, "traffic": traffic,
-                         "peak_basis": f"128 B/clk/SM LDS x {sms} SMs x {fmax:.0f} MHz (guide-derived; no "
-                                       "measured smem peak in MEASURED_PEAKS.json)",
+                         "traffic_source": traffic_src if traffic else None,
+                         "peak_basis": peak_basis, "smem_probe": probe,
+                         "nominal_peak": nominal_gbs, "frac_of_nominal": achieved / nominal_gbs,
                          "evals_per_instance": W / n_inst, "kernel_ms": kern_ms,
                          "work": "W_active evals x 4 B (DESIGN.md §5)",
                          "survey_evals_per_instance": W_survey / n_inst,
@@ -610,6 +693,7 @@ def main():
             "clocks": clk_s,
             "kernel": info,
             "stats": dict(zip(pkg.STATS_FIELDS, [int(x) for x in stats])),
+            "accuracy_and_misses": derived_metrics(stats),
             "result_hash": hex(int(rh.item()) & ((1 << 64) - 1)),
         }
         if e2e:
@@ -617,11 +701,8 @@ def main():
         if latency:
             line["latency"] = latency
         if world == 1 and not args.no_cpu_baseline:
-            v, n, el, thr = cpu_oracle_rate(cw, args, args.cpu_seconds)
-            line["cpu_baseline"] = {"value": v, "unit": "instances/s", "cores": thr, "kind": "oracle",
-                                    "sample": f"{n} {cw.name} instances (" +
-                                              ("equal parts of every U block" if cw.u_blocks else f"ids 0..{n - 1}") +
-                                              f"), paper reward-indexed DP (O2) on {thr} OpenMP threads, {el:.1f} s"}
+            line["cpu_baseline"] = cpu_oracle_baseline(cw, args, args.cpu_seconds)
+        line["paper_context"] = PAPER_CONTEXT
         print(json.dumps(line), flush=True)
     sched.close()
     if world > 1:

@@ -39,8 +39,9 @@
  *   - Host-checkable problems return a negative code immediately and launch
  *     nothing: IC_ERR_INVALID_ARG (null handle / pointer, bad config),
  *     IC_ERR_LIMIT (config beyond the compiled limits: max_tasks > 4096,
- *     max_opt_stages > 14, max_horizon > 32768, or the workspace does not fit
- *     the device), IC_ERR_CUDA (a CUDA runtime call failed; no device at
+ *     max_opt_stages > 14, max_horizon > 32768, or the per-instance tables do
+ *     not fit one SM's 227 KB of shared memory — see "Envelope" below — or the
+ *     workspace does not fit the device), IC_ERR_CUDA (a CUDA runtime call failed; no device at
  *     all also reports this), IC_ERR_OOM (workspace allocation failed).
  *   - Data problems are reported per instance in out->status, never by
  *     return code: IC_INST_BAD_INPUT when an instance has more than
@@ -48,8 +49,9 @@
  *     deadline >= max_horizon, any WCET < 1, mand_conf > 1e6, or a
  *     cumulative confidence R_i(k) outside [0, 1e6];
  *     IC_INST_INFEASIBLE when dropping is disallowed and no plan keeps every
- *     task; IC_INST_LIMIT when 16 * sum_i max_k q_i(k) + 16 * N >= 2^30 (the
- *     packed 32-bit DP keys would overflow; use a larger Delta).  For all
+ *     task; IC_INST_LIMIT when 16 * sum_i max_k q_i(k) + 16 * N >= 2^30, the max
+ *     taken over the depths k that fit alone (r_i + C_i(k) <= d_i) (the packed
+ *     32-bit DP keys would overflow; use a larger Delta).  For all
  *     three, every kept = -1, start = finish = -1, q_total = conf_micro = 0,
  *     conf_total = 0.0, makespan = 0.  There is no fallback path.
  */
@@ -73,7 +75,7 @@ typedef struct {
   uint32_t delta_micro;   /* > 0: fixed Delta in micro-units (paper default 0.1 -> 100000)   */
   uint32_t epsilon_micro; /* iff delta_micro == 0: Delta = max(1, floor(eps*R/(1e6*N))),
                              R = max over tasks/depths with r + C <= d of R_i(k) (Thm 1)    */
-  int32_t max_tasks;      /* N per instance, 1..4096                                        */
+  int32_t max_tasks;      /* N per instance, 1..4096 within the envelope below              */
   int32_t max_opt_stages; /* S_i bound and the row stride of opt_wcet/opt_gain, 0..14       */
   int32_t max_horizon;    /* H: deadlines must be < H; 1..32768                             */
 } ic_sched_config;
@@ -106,7 +108,36 @@ typedef struct {
                           sum conf_micro, sum q_total                                        */
 } ic_batch_out;
 
+/* Envelope.  One SM holds an instance's DP row (4 (H + pad) bytes, pad >= 64 ticks) and
+ * its per-task tables (option table 8 kp bytes per slot with kp = max_opt_stages + 2
+ * rounded down to even, plus ~84 bytes of EDF keys, row headers and staging), with two
+ * table slots when they fit (setup of the next instance overlaps the sweep) and one
+ * otherwise.  So max_tasks is bounded by about (227 KB - 4 (H + pad)) / (8 kp + 52):
+ * e.g. ~1500 tasks at S = 8, H = 4096 and ~500 at S = 14, H = 32768; beyond that
+ * ic_sched_create returns IC_ERR_LIMIT (tests/test_gpu_parity.py::test_create_envelope
+ * finds the boundary). */
 int ic_sched_create(const ic_sched_config* cfg, ic_sched** out);
+
+/* Launch tuning, fixed at create time (A/B measurements and tests that must reach every
+ * kernel variant).  ic_sched_create(cfg, out) == ic_sched_create_tuned(cfg, NULL, out);
+ * a zero field means "the default the library picks".  The library never reads the
+ * process environment.  Results are identical for every valid tuning;
+ * IC_ERR_INVALID_ARG for out-of-range fields. */
+typedef struct {
+  int32_t dp_warps;      /* 1, 2, 4, 8 or 16 DP warps per instance (default: ~32 column groups per thread) */
+  int32_t pad_cols;      /* NEG pad left of column 0 in ticks (default: grown into spare shared memory)      */
+  int32_t in_place;      /* 1: rows updated in place (forces >= 8 DP warps); default only when H needs it     */
+  int32_t slots;         /* 1: setup and sweep serialised (one table slot); default 2 when they fit           */
+  int32_t decisions;     /* 1: decisions in shared memory if they fit; 2: one global buffer; default 2 global */
+  int32_t option_tables; /* 1: option tables of both slots in a per-CTA global slab (>= 8 DP warps)          */
+  int32_t axis;          /* 1: time axis only; 2: reward axis whenever eligible; default per instance         */
+  int32_t ckpt;          /* re-plan checkpoint spacing in rows, power of two (default 4)                     */
+  int32_t ctas_per_sm;   /* cap on resident CTAs per SM (default: occupancy)                                 */
+  int32_t no_vec_loads;  /* 1: scalar descriptor loads only                                                  */
+  int32_t kernel;        /* 1: warp-specialised kernel; 2: one warp per instance; default by shape          */
+} ic_sched_tuning;
+int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_tuning* tuning, ic_sched** out);
+
 int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream);
 int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream);
 int ic_sched_destroy(ic_sched* h);
@@ -160,7 +191,7 @@ int ic_sched_reassign_batch(ic_sched* h, const ic_batch_in* in, const ic_stage_u
  *                                     full ic_sched_solve_batch of the new instances.
  * Requires a fixed Delta (delta_micro > 0: the FPTAS step eps*R/N changes with N) and
  * max_horizon <= 16384 (IC_ERR_INVALID_ARG / IC_ERR_LIMIT otherwise).  Every ckpt-th row
- * is kept (IC_SCHED_CKPT, default 4), so a re-plan restarts at the last kept row before the
+ * is kept (ic_sched_tuning.ckpt, default 4), so a re-plan restarts at the last kept row before the
  * arrival; if the instance's sweep axis changes (time vs reward) it restarts at row 0.
  * Same stream/ownership rules as ic_sched_solve_batch. */
 int64_t ic_sched_state_bytes(const ic_sched* h, int64_t n_instances);

@@ -24,6 +24,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# bench.py's CPU baseline builds a copy tuned for the host it runs on (-march=native) at run
+# time; the portable build is the one the tests load (it travels to the GPU box prebuilt)
+_LIB_NATIVE = os.path.join(_HERE, "liboracle_native.so")
 
 BRUTE, PAPER, TIME = 1, 2, 3
 OK, INFEASIBLE, BAD_INPUT = 0, 1, 2
@@ -56,32 +59,47 @@ class _Out(ctypes.Structure):
                                                "makespan", "status", "delta_used")]
 
 
-def build(force: bool = False) -> str:
+def build(force: bool = False, native: bool = False) -> str:
     src = os.path.join(_HERE, "ic_oracle.c")
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC",
-                               "-o", _LIB_PATH, src])
-    return _LIB_PATH
+    path = _LIB_NATIVE if native else _LIB_PATH
+    if force or native or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+        flags = ["-O3", "-march=native"] if native else ["-O3"]
+        subprocess.check_call(["gcc", *flags, "-std=c11", "-fopenmp", "-shared", "-fPIC", "-o", path, src])
+    return path
 
 
 _lib = None
+
+
+def use_native_build() -> str:
+    """Rebuild the oracle for this host's CPU (-O3 -march=native) and load that copy; used by
+    bench.py's CPU baseline only.  Must run before the first solve."""
+    global _lib
+    assert _lib is None, "oracle already loaded"
+    path = build(native=True)
+    _lib = _bind(ctypes.CDLL(path))
+    return path
 
 
 def _load():
     global _lib
     if _lib is None:
         build()
-        _lib = ctypes.CDLL(_LIB_PATH)
-        _lib.or_solve_batch.argtypes = [ctypes.c_int, ctypes.POINTER(_Cfg), ctypes.POINTER(_In),
-                                        ctypes.POINTER(_Out), ctypes.c_int]
-        _lib.or_solve_batch.restype = ctypes.c_int
-        for f in (_lib.or_paper_table, _lib.or_time_table):
-            f.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(_In), ctypes.c_int64,
-                          ctypes.c_void_p, ctypes.c_int64]
-            f.restype = ctypes.c_int64
-        _lib.or_check.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(_In), ctypes.POINTER(_Out),
-                                  ctypes.c_int64]
-        _lib.or_check.restype = ctypes.c_int
+        _lib = _bind(ctypes.CDLL(_LIB_PATH))
+    return _lib
+
+
+def _bind(_lib):
+    _lib.or_solve_batch.argtypes = [ctypes.c_int, ctypes.POINTER(_Cfg), ctypes.POINTER(_In),
+                                    ctypes.POINTER(_Out), ctypes.c_int]
+    _lib.or_solve_batch.restype = ctypes.c_int
+    for f in (_lib.or_paper_table, _lib.or_time_table):
+        f.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(_In), ctypes.c_int64,
+                      ctypes.c_void_p, ctypes.c_int64]
+        f.restype = ctypes.c_int64
+    _lib.or_check.argtypes = [ctypes.POINTER(_Cfg), ctypes.POINTER(_In), ctypes.POINTER(_Out),
+                              ctypes.c_int64]
+    _lib.or_check.restype = ctypes.c_int
     return _lib
 
 

@@ -19,8 +19,8 @@ from .abi import (  # noqa: F401
     IC_INST_OK, IC_INST_INFEASIBLE, IC_INST_BAD_INPUT, IC_INST_LIMIT,
     IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN,
     INPUT_FIELDS, OUTPUT_FIELDS, STATS_FIELDS,
-    SchedConfig, SchedInfo, Scheduler, ICSchedError, lib_path, load_library,
+    SchedConfig, SchedInfo, SchedTuning, TUNING_FIELDS, Scheduler, use_library, ICSchedError, lib_path, load_library,
     alloc_inputs, alloc_outputs, gen_batch_device,
     IC_SIM_PLANNER, IC_SIM_EDF, IC_SIM_LCF, IC_SIM_RR, IC_SIM_UTIL_EXP, IC_SIM_UTIL_ORACLE,
-    SimConfig, SimResult, simulate,
+    SimConfig, SimResult, simulate, probe_smem,
 )

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.environ.get("IC_SCHED_LIB") or os.path.join(_HERE, "libicsched.so")  # override: A/B builds only
+_LIB = os.path.join(_HERE, "libicsched.so")
 
 IC_OK, IC_ERR_INVALID_ARG, IC_ERR_LIMIT, IC_ERR_CUDA, IC_ERR_OOM = 0, -1, -2, -3, -4
 IC_DROP_ALLOWED, IC_MANDATORY_ENFORCED = 0, 1
@@ -51,6 +51,21 @@ class SchedConfig(ctypes.Structure):
                          max_horizon)
 
 
+TUNING_FIELDS = ("dp_warps", "pad_cols", "in_place", "slots", "decisions", "option_tables", "axis", "ckpt",
+                 "ctas_per_sm", "no_vec_loads", "kernel")
+
+
+class SchedTuning(ctypes.Structure):
+    """include/ic_sched.h ic_sched_tuning: launch choices fixed at create (0 = library default)."""
+    _fields_ = [(n, ctypes.c_int32) for n in TUNING_FIELDS]
+
+    def __init__(self, **kw):
+        bad = set(kw) - set(TUNING_FIELDS)
+        if bad:
+            raise ValueError(f"unknown tuning fields {sorted(bad)}")
+        super().__init__(*[int(kw.get(n, 0)) for n in TUNING_FIELDS])
+
+
 class SchedInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("threads_per_cta", "cols_per_thread", "ctas_per_sm", "grid",
                                               "smem_bytes", "decisions_in_smem", "double_buffered",
@@ -74,9 +89,9 @@ class _GenCfg(ctypes.Structure):
                 ("u_hi_q16", ctypes.c_int32), ("d_lo", ctypes.c_int32), ("release_mode", ctypes.c_int32)]
 
 
-EXPORTED = ("ic_sched_create", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
+EXPORTED = ("ic_sched_create", "ic_sched_create_tuned", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
             "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch", "ic_sched_state_bytes",
-            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sim_run")
+            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sim_run", "ic_probe_smem")
 
 IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
 
@@ -128,11 +143,33 @@ def simulate(cfg: SimConfig) -> dict:
     return r.as_dict()
 
 
+PROBE_MODES = {"lds32": 0, "lds128": 1, "lds32_viaddmax": 2}
+
+
+def probe_smem(device: int = 0, mode: str = "lds32", target_ms: float = 50.0) -> dict:
+    """ic_probe_smem (include/ic_probe.h): measured shared-memory load bandwidth of `device`."""
+    lib = load_library()
+    bps, bpc = ctypes.c_double(), ctypes.c_double()
+    rc = lib.ic_probe_smem(device, PROBE_MODES[mode], target_ms, ctypes.byref(bps), ctypes.byref(bpc))
+    if rc != 0:
+        raise ICSchedError("ic_probe_smem", rc)
+    return {"mode": mode, "gbs": bps.value / 1e9, "bytes_per_clk_per_sm": bpc.value}
+
+
 _lib = None
 
 
 def lib_path() -> str:
     return _LIB
+
+
+def use_library(path: str) -> None:
+    """Load the library from an explicit path instead of the in-tree build (A/B comparisons
+    of two builds in tools/ and bench.py --lib).  Must be called before the first load."""
+    global _LIB
+    if _lib is not None and os.path.abspath(path) != _LIB:
+        raise RuntimeError("libicsched already loaded from " + _LIB)
+    _LIB = os.path.abspath(path)
 
 
 def load_library():
@@ -145,6 +182,7 @@ def load_library():
         lib = ctypes.CDLL(_LIB)
         P = ctypes.POINTER
         lib.ic_sched_create.argtypes = [P(SchedConfig), P(ctypes.c_void_p)]
+        lib.ic_sched_create_tuned.argtypes = [P(SchedConfig), P(SchedTuning), P(ctypes.c_void_p)]
         lib.ic_sched_solve_batch.argtypes = [ctypes.c_void_p, P(_In), P(_Out), ctypes.c_void_p]
         lib.ic_sched_solve_batch_host.argtypes = [ctypes.c_void_p, P(_In), P(_Out), ctypes.c_void_p]
         lib.ic_sched_destroy.argtypes = [ctypes.c_void_p]
@@ -158,11 +196,18 @@ def load_library():
         lib.ic_sched_replan_batch.argtypes = [ctypes.c_void_p, P(_In), ctypes.c_void_p, P(_Out), ctypes.c_void_p]
         lib.ic_sched_state_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         lib.ic_sim_run.argtypes = [P(SimConfig), P(SimResult)]
+        lib.ic_probe_smem.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P(ctypes.c_double),
+                                      P(ctypes.c_double)]
         for f in EXPORTED:
             getattr(lib, f).restype = ctypes.c_int
         lib.ic_sched_state_bytes.restype = ctypes.c_int64
         _lib = lib
     return _lib
+
+
+def _torch_dtype(dt):
+    import torch
+    return torch.from_numpy(np.zeros(0, dt)).dtype
 
 
 def _ptr(x):
@@ -200,11 +245,16 @@ def alloc_outputs(n_instances: int, n_tasks: int, device="cuda", pinned: bool = 
 class Scheduler:
     """One ic_sched handle (bound to a device; one stream at a time)."""
 
-    def __init__(self, cfg: SchedConfig):
+    def __init__(self, cfg: SchedConfig, tuning: SchedTuning | dict | None = None):
         self._lib = load_library()
         self.cfg = cfg
         h = ctypes.c_void_p()
-        rc = self._lib.ic_sched_create(ctypes.byref(cfg), ctypes.byref(h))
+        if tuning is None:
+            rc = self._lib.ic_sched_create(ctypes.byref(cfg), ctypes.byref(h))
+        else:
+            if isinstance(tuning, dict):
+                tuning = SchedTuning(**tuning)
+            rc = self._lib.ic_sched_create_tuned(ctypes.byref(cfg), ctypes.byref(tuning), ctypes.byref(h))
         if rc != IC_OK:
             raise ICSchedError("ic_sched_create", rc)
         self._h = h
@@ -216,7 +266,41 @@ class Scheduler:
             raise ICSchedError("ic_sched_get_info", rc)
         return i.as_dict()
 
+    def _check(self, inputs, outputs):
+        """Layout checks the C ABI cannot make: dtype, contiguity, one device, and the
+        (T, max_opt_stages) row stride of the optional-stage arrays (the kernel indexes
+        row t at t * max_opt_stages, so any other stride would read the wrong stages)."""
+        dev = None
+        B = _n_instances(inputs)
+        for fields, bufs in ((INPUT_FIELDS, inputs), (OUTPUT_FIELDS, outputs)):
+            for name, dt, kind in fields:
+                x = bufs[name]
+                if hasattr(x, "data_ptr"):
+                    ok_dt = x.dtype == _torch_dtype(dt)
+                    contig = x.is_contiguous()
+                    d = str(x.device)
+                    shape = tuple(x.shape)
+                else:
+                    ok_dt = x.dtype == np.dtype(dt)
+                    contig = x.flags.c_contiguous
+                    d = "cpu"
+                    shape = x.shape
+                if not ok_dt:
+                    raise TypeError(f"{name}: dtype {x.dtype}, expected {np.dtype(dt)}")
+                if not contig:
+                    raise ValueError(f"{name}: must be contiguous")
+                if dev is None:
+                    dev = d
+                elif d != dev:
+                    raise ValueError(f"{name}: on {d}, other buffers on {dev}")
+                if kind == "task_opt" and (len(shape) != 2 or shape[1] != self.cfg.max_opt_stages):
+                    raise ValueError(f"{name}: shape {shape}, expected (T, {self.cfg.max_opt_stages})")
+                if kind == "instance" and shape[0] < B:
+                    raise ValueError(f"{name}: {shape[0]} entries for {B} instances")
+        return dev
+
     def _marshal(self, inputs, outputs):
+        self._check(inputs, outputs)
         i = _In(_n_instances(inputs), *[_ptr(inputs[n]) for n, _, _ in INPUT_FIELDS])
         o = _Out(*[_ptr(outputs[n]) for n, _, _ in OUTPUT_FIELDS], _ptr(outputs.get("stats")))
         return i, o

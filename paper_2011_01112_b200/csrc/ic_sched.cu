@@ -99,41 +99,50 @@ struct ic_sched {
   cudaEvent_t ev[3 * 4 + 2];
   int64_t* tb_pinned;  // [3][chunk+1] rebased CSR offsets of the staged chunks
   int64_t tb_cap;
+  int axis_mode;       // tuning, fixed at create: 0 auto per instance, 1 time, 2 reward
+  int ckpt;            // re-plan checkpoint spacing (rows), power of two
+  int no_vec_loads;    // 1: scalar descriptor loads only
 };
 
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
+extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
+  return ic_sched_create_tuned(cfg, nullptr, out);
 }
 
-extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
+extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_tuning* tuning, ic_sched** out) {
   if (!cfg || !out) return IC_ERR_INVALID_ARG;
   *out = nullptr;
   const ic_sched_config c = *cfg;
+  ic_sched_tuning tu{};
+  if (tuning) tu = *tuning;
   if (c.drop_mode != IC_DROP_ALLOWED && c.drop_mode != IC_MANDATORY_ENFORCED) return IC_ERR_INVALID_ARG;
   if (c.delta_micro == 0 && c.epsilon_micro == 0) return IC_ERR_INVALID_ARG;
   if (c.max_tasks < 1 || c.max_opt_stages < 0 || c.max_horizon < 1) return IC_ERR_INVALID_ARG;
   if (c.max_tasks > kMaxTasks || c.max_opt_stages > kMaxOpt || c.max_horizon > kMaxHorizon)
     return IC_ERR_LIMIT;
+  if (tu.dp_warps < 0 || tu.pad_cols < 0 || tu.in_place < 0 || tu.in_place > 1 || tu.slots < 0 || tu.slots > 2 ||
+      tu.decisions < 0 || tu.decisions > 2 || tu.option_tables < 0 || tu.option_tables > 1 || tu.axis < 0 ||
+      tu.axis > 2 || tu.ckpt < 0 || (tu.ckpt & (tu.ckpt - 1)) != 0 || tu.ctas_per_sm < 0 || tu.no_vec_loads < 0 ||
+      tu.no_vec_loads > 1 || tu.kernel < 0 || tu.kernel > 2)
+    return IC_ERR_INVALID_ARG;
   if (cudaSetDevice(c.device) != cudaSuccess) return IC_ERR_CUDA;
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device) != cudaSuccess)
     return IC_ERR_CUDA;
   const bool drop = c.drop_mode == IC_DROP_ALLOWED;
 
-  // DP warps per instance: about 32 column groups per thread (IC_SCHED_NW overrides).
+  // DP warps per instance: about 32 column groups per thread (tuning.dp_warps overrides).
   int nw = 1;
   while (nw < 16 && 32 * nw * 32 < c.max_horizon) nw *= 2;
-  nw = env_int("IC_SCHED_NW", nw);
+  if (tu.dp_warps) nw = tu.dp_warps;
   if (nw != 1 && nw != 2 && nw != 4 && nw != 8 && nw != 16) return IC_ERR_INVALID_ARG;
   // NEG pad left of column 0: rows whose longest usable option reaches further use
   // the masked general path, so the pad only trades shared memory for speed.
   int pad = c.max_horizon / 16 < 64 ? 64 : (c.max_horizon / 16 > 256 ? 256 : c.max_horizon / 16);
   if (pad > c.max_horizon) pad = c.max_horizon;
-  pad = env_int("IC_SCHED_PAD", pad);
+  if (tu.pad_cols) pad = tu.pad_cols;
   pad = (pad + 31) & ~31;
 
-  bool sb = env_int("IC_SCHED_SB", 0) != 0;  // in-place rows (tests force it at small H)
+  bool sb = tu.in_place != 0;  // in-place rows (tests force it at small H)
   if (sb && nw < 8) nw = 8;
   Layout Lg = make_layout(c, nw, sb, pad, false);
   if (!sb && Lg.bytes > kSmemLimit) {
@@ -141,11 +150,10 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
     if (nw < 8) nw = 8;
     Lg = make_layout(c, nw, true, pad, false);
   }
-  int nslots = env_int("IC_SCHED_SLOTS", 2) == 1 ? 1 : 2;
+  int nslots = tu.slots == 1 ? 1 : 2;
   // large task sets: keep both slots' option tables in a global (L2) slab so the setup
-  // and backtrack still overlap the sweep (IC_SCHED_ROWP=global forces it for tests)
-  const char* rowp_env = getenv("IC_SCHED_ROWP");
-  int rowp_global = rowp_env && !strcmp(rowp_env, "global") ? 1 : 0;
+  // and backtrack still overlap the sweep (tuning.option_tables = 1 forces it for tests)
+  int rowp_global = tu.option_tables;
   if (nslots == 2 && nw >= 8 && (Lg.bytes > kSmemLimit || rowp_global)) {  // compiled for NW >= 8 only
     rowp_global = 1;
     Lg = make_layout(c, nw, sb, pad, false, 2, 1, 1);
@@ -157,16 +165,15 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   }
   if (Lg.bytes > kSmemLimit) return IC_ERR_LIMIT;
   // decisions: a global (L2-resident) double buffer by default, so the backtrack of
-  // instance b overlaps the sweep of b+1; IC_SCHED_DEC=smem keeps one buffer in smem.
+  // instance b overlaps the sweep of b+1; tuning.decisions = 1 keeps one buffer in smem.
   int ndec = nslots == 2 ? 2 : 1;
   bool dec_smem = false;
-  const char* env = getenv("IC_SCHED_DEC");
-  if (env && !strcmp(env, "smem")) {
+  if (tu.decisions == 1) {
     Layout Ls = make_layout(c, nw, sb, pad, true, nslots, 1, rowp_global);
     dec_smem = Ls.bytes <= kSmemLimit;
     if (dec_smem) ndec = 1;
   }
-  if (env && !strcmp(env, "global1")) ndec = 1;
+  if (tu.decisions == 2) ndec = 1;
   Layout L = make_layout(c, nw, sb, pad, dec_smem, nslots, ndec, rowp_global);
 
   KernelFn fn = kernel_for(nw, sb, drop);
@@ -179,7 +186,7 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   if (per_sm < 1) return IC_ERR_LIMIT;
   // Spend the shared memory the occupancy leaves over on a wider pad: rows whose options
   // reach past it take the (slower) edge path for their first chunk.
-  if (!getenv("IC_SCHED_PAD")) {
+  if (!tu.pad_cols) {
     for (int p2 = pad + 32; p2 <= c.max_horizon; p2 += 32) {
       const Layout L2 = make_layout(c, nw, sb, p2, dec_smem, nslots, ndec, rowp_global);
       int o2 = 0;
@@ -190,7 +197,7 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
       L = L2;
     }
   }
-  per_sm = env_int("IC_SCHED_CTAS", per_sm) < per_sm ? env_int("IC_SCHED_CTAS", per_sm) : per_sm;
+  if (tu.ctas_per_sm && tu.ctas_per_sm < per_sm) per_sm = tu.ctas_per_sm;
 
   ic_sched* h = (ic_sched*)calloc(1, sizeof(ic_sched));
   if (!h) return IC_ERR_OOM;
@@ -203,6 +210,9 @@ extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
   h->sms = sms;
   h->ctas_per_sm = per_sm;
   h->grid = sms * per_sm;
+  h->axis_mode = tu.axis;
+  h->ckpt = tu.ckpt ? tu.ckpt : 4;
+  h->no_vec_loads = tu.no_vec_loads;
   if (cudaMalloc(&h->work, 16) != cudaSuccess || cudaMemset(h->work, 0, 16) != cudaSuccess) {
     free(h);
     return IC_ERR_OOM;
@@ -272,12 +282,8 @@ static int check_io(const ic_batch_in* in, const ic_batch_out* out) {
   return IC_OK;
 }
 
-static int state_ckpt() {  // checkpoint every c-th DP row (power of two; IC_SCHED_CKPT overrides)
-  int c = env_int("IC_SCHED_CKPT", 4);
-  return c >= 1 && (c & (c - 1)) == 0 ? c : 4;
-}
-static int64_t state_rows_bytes(const ic_sched* h) {
-  return (int64_t)(h->cfg.max_tasks / state_ckpt() + 1) * (h->cfg.max_horizon + 1) * 4;
+static int64_t state_rows_bytes(const ic_sched* h) {  // every ckpt-th DP row (fixed at create)
+  return (int64_t)(h->cfg.max_tasks / h->ckpt + 1) * (h->cfg.max_horizon + 1) * 4;
 }
 static int64_t state_dec_bytes(const ic_sched* h) { return (int64_t)h->cfg.max_tasks * h->L.nq * 32 * h->nw * 4; }
 static int64_t state_stride(const ic_sched* h) {
@@ -375,20 +381,20 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.cap = L.cap;
   p.off_aux = L.off_aux;
   p.off_sQ = L.off_sQ;
-  p.axis_mode = env_int("IC_SCHED_AXIS", 0);
+  p.axis_mode = h->axis_mode;
   p.state = (char*)state;
   p.state_stride = state_stride(h);
   p.state_dec_off = state_rows_bytes(h);
   p.state_tail_off = state_rows_bytes(h) + state_dec_bytes(h);
   p.replan = replan;
-  p.ckpt = state_ckpt();
+  p.ckpt = h->ckpt;
   p.work = h->work;
   p.ndec = L.ndec;
   p.dec_words = (int64_t)h->cfg.max_tasks * L.nq * 32 * h->nw;
   p.rowp_g = h->rowp_g;
   p.rowp_slab = h->rowp_slab;
   p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
-               ((uintptr_t)p.opt_gain & 15) == 0 && !getenv("IC_SCHED_NOVEC");
+               ((uintptr_t)p.opt_gain & 15) == 0 && !h->no_vec_loads;
   int64_t grid = h->grid;
   if (grid > in->n_instances) grid = in->n_instances;
   h->fn<<<(unsigned)grid, 32 * (h->nw + 1), h->L.bytes, (cudaStream_t)cuda_stream>>>(p);
@@ -427,6 +433,7 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
   int rc = check_io(in, out);
   if (rc != IC_OK) return rc;
   if (in->n_instances == 0) return IC_OK;
+  if (h->cfg.max_opt_stages > 0 && (!in->opt_wcet || !in->opt_gain)) return IC_ERR_INVALID_ARG;
   if (cudaSetDevice(h->cfg.device) != cudaSuccess) return IC_ERR_CUDA;
   if (!h->s_in) {
     if (cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking) != cudaSuccess ||
@@ -480,6 +487,14 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
   }
   char* g0 = (char*)h->stage;
   cudaStream_t user = (cudaStream_t)cuda_stream;
+  // every early return first drains the three pipeline streams, so no copy still in flight
+  // touches the caller's host buffers or the pinned CSR ring after the call returns
+  auto fail = [&](int code) {
+    cudaStreamSynchronize(h->s_in);
+    cudaStreamSynchronize(h->s_comp);
+    cudaStreamSynchronize(h->s_out);
+    return code;
+  };
   cudaEvent_t* ev = h->ev;  // [slot*4 + 0] inputs staged, +1 kernel done, +2 outputs drained; [12], [13]
   bool ok = cudaEventRecord(ev[13], user) == cudaSuccess &&
             cudaStreamWaitEvent(h->s_in, ev[13], 0) == cudaSuccess &&
@@ -492,7 +507,7 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
     const int sl = (int)(j % 3);
     char* g = g0 + sl * slot;
     if (j >= 3) {  // slot reuse: its previous chunk's outputs must be drained, its CSR copied
-      if (cudaEventSynchronize(ev[sl * 4 + 2]) != cudaSuccess) return IC_ERR_CUDA;
+      if (cudaEventSynchronize(ev[sl * 4 + 2]) != cudaSuccess) return fail(IC_ERR_CUDA);
       ok = cudaStreamWaitEvent(h->s_in, ev[sl * 4 + 2], 0) == cudaSuccess;
     }
     int64_t* tbp = h->tb_pinned + sl * (chunk + 1);
@@ -515,7 +530,7 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
                          (int64_t*)(g + o_c), (double*)(g + o_ct), (int32_t*)(g + o_ms), (uint8_t*)(g + o_st),
                          out->stats ? (int64_t*)(g0 + o_stats) : nullptr};
     rc = ic_sched_solve_batch(h, &din, &dout, h->s_comp);
-    if (rc != IC_OK) return rc;
+    if (rc != IC_OK) return fail(rc);
     ok = cudaEventRecord(ev[sl * 4 + 1], h->s_comp) == cudaSuccess &&
          cudaStreamWaitEvent(h->s_out, ev[sl * 4 + 1], 0) == cudaSuccess;
     auto d2h = [&](void* dst, size_t o, size_t bytes) {
@@ -532,7 +547,8 @@ extern "C" int ic_sched_solve_batch_host(ic_sched* h, const ic_batch_in* in, ic_
     ok = cudaEventRecord(ev[12], h->s_comp) == cudaSuccess && cudaStreamWaitEvent(h->s_out, ev[12], 0) == cudaSuccess &&
          cudaMemcpyAsync(stats_dev, g0 + o_stats, 64, cudaMemcpyDeviceToHost, h->s_out) == cudaSuccess;
   }
-  if (cudaStreamSynchronize(h->s_out) != cudaSuccess || !ok) return IC_ERR_CUDA;
+  if (!ok) return fail(IC_ERR_CUDA);
+  if (cudaStreamSynchronize(h->s_out) != cudaSuccess) return fail(IC_ERR_CUDA);
   if (out->stats)
     for (int i = 0; i < 8; ++i) out->stats[i] += stats_dev[i];
   return IC_OK;

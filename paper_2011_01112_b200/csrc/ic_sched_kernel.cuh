@@ -496,9 +496,9 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
       long long C = p.mand_wcet[t], R = p.mand_conf[t];
       auto option = [&](int k) {
-        const int q = (int)(R / delta);
-        qmax = max(qmax, q);
-        if (C <= (long long)d - r) {  // options that can fit (C increasing in k)
+        if (C <= (long long)d - r) {  // options that can fit (C increasing in k); only they
+          const int q = (int)(R / delta);  // bound the packed keys and the reward columns
+          qmax = max(qmax, q);
           rp[k] = make_int2((int)C, (q << 4) - (k + 1));
           K = k + 1;
         }

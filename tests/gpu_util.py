@@ -14,13 +14,14 @@ def to_device(batch):
     return {f: torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).cuda() for f, _, _ in pkg.INPUT_FIELDS}
 
 
-def gpu_solve(batch, *, max_tasks, max_opt, max_horizon, drop_mode=0, delta=0, eps=100_000, host=False):
+def gpu_solve(batch, *, max_tasks, max_opt, max_horizon, drop_mode=0, delta=0, eps=100_000, host=False,
+              tuning=None):
     import torch
     import paper_2011_01112_b200 as pkg
     assert batch.opt_stride == max_opt
     sc = pkg.SchedConfig(max_tasks=max_tasks, max_opt_stages=max_opt, max_horizon=max_horizon,
                          drop_mode=drop_mode, delta_micro=delta, epsilon_micro=eps)
-    with pkg.Scheduler(sc) as s:
+    with pkg.Scheduler(sc, tuning) as s:
         if host:
             inp = {f: np.ascontiguousarray(getattr(batch, f)) for f, _, _ in pkg.INPUT_FIELDS}
             out = pkg.alloc_outputs(batch.n_instances, batch.n_total_tasks, host=True, pinned=True)

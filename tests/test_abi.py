@@ -18,7 +18,8 @@ def _declared(header):
 
 def test_library_exports_every_declared_symbol():
     lib = pkg.load_library()
-    declared = _declared("ic_sched.h") | _declared("ic_sim.h") | (_declared("ic_gen.h") - {"ic_gen_batch_host"})
+    declared = (_declared("ic_sched.h") | _declared("ic_sim.h") | _declared("ic_probe.h")
+                | (_declared("ic_gen.h") - {"ic_gen_batch_host"}))
     assert declared == set(pkg.abi.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name

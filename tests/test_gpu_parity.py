@@ -167,62 +167,28 @@ def test_device_generator_matches_host():
             np.testing.assert_array_equal(dev[f].cpu().numpy(), getattr(host, f), err_msg=f)
 
 
-def test_decisions_in_global_memory(monkeypatch):
-    """The global-slab decision store gives identical results."""
-    monkeypatch.setenv("IC_SCHED_DEC", "global")
+@pytest.mark.parametrize("decisions", [0, 1, 2])
+def test_decision_placement(decisions):
+    """Decisions in the global double buffer (default), in shared memory, or one global buffer
+    give identical results."""
     cw = gen.CONFIGS["C2"]
     batch = gen.generate(cw, 300)
     ref = oracle.solve(batch, OracleConfig(epsilon_micro=100_000, max_tasks=32, max_horizon=1024), PAPER)
-    got = gpu_solve(batch, max_tasks=32, max_opt=4, max_horizon=1024)
-    assert got["_info"]["decisions_in_smem"] == 0
-    assert_parity(got, ref, "global decisions")
+    got = gpu_solve(batch, max_tasks=32, max_opt=4, max_horizon=1024, tuning=dict(decisions=decisions))
+    assert got["_info"]["decisions_in_smem"] == (1 if decisions == 1 else 0)
+    assert_parity(got, ref, f"decisions={decisions}")
 
 
-@pytest.mark.parametrize("name,sample", [("C2", 97), ("C3", 2003), ("C4", 2503)])
-def test_full_size_sampled(name, sample):
-    """BASELINE.json full sizes in the bench launch configuration (device-generated inputs);
-    a deterministic sample is checked element by element against the oracle, every instance by
-    the invariant checker (C2) and the stats vector against the outputs."""
-    import paper_2011_01112_b200 as pkg
-    cw = gen.CONFIGS[name]
-    gc = cw.gen_config()
-    B = cw.n_instances
-    dev = pkg.gen_batch_device(gc.seed, gc.n_tasks, gc.n_opt, gc.opt_stride, gc.horizon, gc.u_lo_q16,
-                               gc.u_hi_q16, gc.d_lo, B)
-    sc = pkg.SchedConfig(max_tasks=cw.n_tasks, max_opt_stages=cw.n_opt, max_horizon=cw.horizon,
-                         epsilon_micro=cw.epsilon_micro)
-    with pkg.Scheduler(sc) as s:
-        out = s.solve_batch(dev)
-        torch.cuda.synchronize()
-    got = {k: v.cpu().numpy() for k, v in out.items()}
-    N = cw.n_tasks
-    idx = np.arange(0, B, sample)
-    parts = [gen.generate(cw, 1, id_offset=int(b)) for b in idx]
-    sub = gen.concat(parts, cw.n_opt)
-    ocfg = OracleConfig(epsilon_micro=cw.epsilon_micro, max_tasks=N, max_horizon=cw.horizon)
-    ref = oracle.solve(sub, ocfg, TIME)
-    tmask = (np.arange(B * N).reshape(B, N)[idx]).ravel()
-    picked = {k: (got[k][tmask] if k in ("kept", "start", "finish") else got[k][idx])
-              for k in ("kept", "start", "finish", "q_total", "conf_micro", "conf_total", "makespan", "status")}
-    assert_parity(picked, ref, f"{name} sampled")
-    assert got["stats"][0] == B
-    assert got["stats"][6] == got["conf_micro"].sum() and got["stats"][7] == got["q_total"].sum()
-
-
-@pytest.mark.parametrize("env", [{"IC_SCHED_NW": "1"}, {"IC_SCHED_NW": "2", "IC_SCHED_DEC": "global"},
-                                 {"IC_SCHED_NW": "4"}, {"IC_SCHED_NW": "8", "IC_SCHED_DEC": "global"},
-                                 {"IC_SCHED_NW": "16"}, {"IC_SCHED_SB": "1", "IC_SCHED_NW": "8"},
-                                 {"IC_SCHED_SB": "1", "IC_SCHED_NW": "16", "IC_SCHED_DEC": "global"},
-                                 {"IC_SCHED_PAD": "32"}, {"IC_SCHED_SLOTS": "1", "IC_SCHED_NW": "2"},
-                                 {"IC_SCHED_SLOTS": "1", "IC_SCHED_SB": "1", "IC_SCHED_NW": "8"},
-                                 {"IC_SCHED_ROWP": "global", "IC_SCHED_NW": "8"},
-                                 {"IC_SCHED_ROWP": "global", "IC_SCHED_SB": "1", "IC_SCHED_NW": "16"},
-                                 {"IC_SCHED_ROWP": "global", "IC_SCHED_NW": "8", "IC_SCHED_DEC": "global1"}])
+@pytest.mark.parametrize("tuning", [dict(dp_warps=1), dict(dp_warps=2), dict(dp_warps=4), dict(dp_warps=8),
+                                    dict(dp_warps=16), dict(in_place=1, dp_warps=8), dict(in_place=1, dp_warps=16),
+                                    dict(pad_cols=32), dict(slots=1, dp_warps=2),
+                                    dict(slots=1, in_place=1, dp_warps=8), dict(option_tables=1, dp_warps=8),
+                                    dict(option_tables=1, in_place=1, dp_warps=16),
+                                    dict(option_tables=1, dp_warps=8, decisions=2), dict(no_vec_loads=1),
+                                    dict(decisions=1, dp_warps=2)])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_every_kernel_variant(monkeypatch, env, mode):
+def test_every_kernel_variant(tuning, mode):
     """Every compiled (DP warps, in-place rows, drop mode, decision placement) variant agrees."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
     rng = np.random.default_rng(11 + mode)
     parts = [gen.generate("C3", 40)]
     tiny = gen.tiny_random(rng, 400, max_tasks=6, max_opt=8, horizon=4096)
@@ -233,8 +199,8 @@ def test_every_kernel_variant(monkeypatch, env, mode):
     batch = gen.concat(parts, 8)
     ocfg = OracleConfig(drop_mode=mode, epsilon_micro=100_000, max_tasks=64, max_horizon=4096)
     ref = oracle.solve(batch, ocfg, TIME)
-    got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode)
-    assert_parity(got, ref, f"variant {env} mode={mode}")
+    got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode, tuning=tuning)
+    assert_parity(got, ref, f"variant {tuning} mode={mode}")
 
 
 def test_c5_sweep_blocks():
@@ -253,36 +219,35 @@ def test_c5_sweep_blocks():
     assert np.mean(drops[-12:]) > np.mean(drops[:12])
 
 
-@pytest.mark.parametrize("axis", ["1", "2"])
+@pytest.mark.parametrize("axis", [1, 2])
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("delta", [100_000, 20_000, 0])
-def test_reward_axis(monkeypatch, axis, mode, delta):
-    """NEXT-1: the reward-indexed sweep (the paper's P(i, r) table, forced with IC_SCHED_AXIS=2)
-    and the time axis (IC_SCHED_AXIS=1) give the same canonical plans; instances with releases
+def test_reward_axis(axis, mode, delta):
+    """NEXT-1: the reward-indexed sweep (the paper's P(i, r) table, forced with tuning axis=2)
+    and the time axis (axis=1) give the same canonical plans; instances with releases
     stay on the time axis."""
-    monkeypatch.setenv("IC_SCHED_AXIS", axis)
     rng = np.random.default_rng(31 + mode + delta)
     parts = [gen.tiny_random(rng, 6000, max_tasks=6, max_opt=3, horizon=40, p_release=0.0),
              gen.tiny_random(rng, 500, max_tasks=6, max_opt=3, horizon=40, p_release=0.5)]
     batch = gen.concat(parts, 3)
     ocfg = OracleConfig(drop_mode=mode, delta_micro=delta, epsilon_micro=300_000, max_tasks=6, max_horizon=40)
     ref = oracle.solve(batch, ocfg, BRUTE)
-    got = gpu_solve(batch, max_tasks=6, max_opt=3, max_horizon=40, drop_mode=mode, delta=delta, eps=300_000)
+    got = gpu_solve(batch, max_tasks=6, max_opt=3, max_horizon=40, drop_mode=mode, delta=delta, eps=300_000,
+                    tuning=dict(axis=axis))
     assert_parity(got, ref, f"axis={axis} mode={mode} delta={delta}")
 
 
 @pytest.mark.parametrize("name", ["C2", "C3", "C4"])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_reward_axis_paper_delta(monkeypatch, name, mode):
+def test_reward_axis_paper_delta(name, mode):
     """At the paper's Delta = 0.1 the reward axis is the shorter sweep and is auto-selected."""
     cw = gen.CONFIGS[name]
     batch = gen.generate(cw, {"C2": 300, "C3": 60, "C4": 2}[name])
     ocfg = OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=cw.n_tasks, max_horizon=cw.horizon)
     ref = oracle.solve(batch, ocfg, TIME)
-    for axis in ("0", "1", "2"):
-        monkeypatch.setenv("IC_SCHED_AXIS", axis)
+    for axis in (0, 1, 2):
         got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
-                        delta=100_000)
+                        delta=100_000, tuning=dict(axis=axis))
         assert_parity(got, ref, f"{name} axis={axis} mode={mode}")
 
 
@@ -338,15 +303,14 @@ def _first_tasks(batch, counts):
     return gen.concat(parts, batch.opt_stride)
 
 
-@pytest.mark.parametrize("ckpt", ["1", "4"])
+@pytest.mark.parametrize("ckpt", [1, 4])
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("shape", ["C2", "tiny"])
-def test_incremental_replan(monkeypatch, shape, mode, ckpt):
+def test_incremental_replan(shape, mode, ckpt):
     """NEXT-2 (Alg. 1 from row k): chained arrivals re-planned from the
     state equal a full solve of the grown task set (GPU and oracle)."""
     import paper_2011_01112_b200 as pkg
     from tests.gpu_util import to_device
-    monkeypatch.setenv("IC_SCHED_CKPT", ckpt)
     rng = np.random.default_rng(70 + mode)
     if shape == "C2":
         cw = gen.WorkloadConfig("C2x", 0, 34, 4, 1024, 0.6, 1.0, 35, 0x2011011102)
@@ -361,7 +325,7 @@ def test_incremental_replan(monkeypatch, shape, mode, ckpt):
         full = full.select(np.nonzero(keep)[0])
         base = np.diff(full.task_begin) - 3
     sc = pkg.SchedConfig(max_tasks=mt, max_opt_stages=mo, max_horizon=H, delta_micro=100_000, drop_mode=mode)
-    with pkg.Scheduler(sc) as s:
+    with pkg.Scheduler(sc, dict(ckpt=ckpt)) as s:
         state = torch.zeros(s.state_bytes(full.n_instances), dtype=torch.uint8, device="cuda")
         b0 = _first_tasks(full, base)
         s.solve_batch_state(to_device(b0), state)
@@ -373,3 +337,43 @@ def test_incremental_replan(monkeypatch, shape, mode, ckpt):
             ref = oracle.solve(bk, OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=mt, max_horizon=H),
                                TIME)
             assert_parity(got, ref, f"{shape} arrival {add} mode={mode}")
+
+
+def test_limit_counts_only_options_that_fit():
+    """IC_INST_LIMIT bounds the packed keys by the depths the DP can add (r + C <= d): an
+    instance whose huge-q depths can never fit is solved normally."""
+    fit = dict(r=0, d=10, m=1, w=[50], g=[999_000], a0=1_000)   # the optional stage never fits
+    batch = batch_from_tasks([fit] * 70)
+    got = gpu_solve(batch, max_tasks=70, max_opt=1, max_horizon=64, delta=1)
+    ref = oracle.solve(batch, OracleConfig(delta_micro=1, max_tasks=70, max_horizon=64), TIME)
+    assert got["status"][0] == 0
+    assert_parity(got, ref, "limit over fitting depths")
+
+
+@pytest.mark.parametrize("S,H,lo,hi", [(8, 4096, 1024, 2048), (14, 32768, 256, 1024)])
+def test_create_envelope(S, H, lo, hi):
+    """include/ic_sched.h "Envelope": the largest max_tasks ic_sched_create accepts lies in the
+    documented band; one task more is IC_ERR_LIMIT, and a solve at the boundary is correct."""
+    import paper_2011_01112_b200 as pkg
+    def ok(n):
+        try:
+            pkg.Scheduler(pkg.SchedConfig(max_tasks=n, max_opt_stages=S, max_horizon=H)).close()
+            return True
+        except pkg.ICSchedError as e:
+            assert e.rc == pkg.IC_ERR_LIMIT
+            return False
+    a, b = 1, 4097
+    while b - a > 1:
+        m = (a + b) // 2
+        a, b = (m, b) if ok(m) else (a, m)
+    assert lo <= a < hi, a
+    assert not ok(a + 1)
+    rng = np.random.default_rng(3)
+    tiny = gen.tiny_random(rng, 3, max_tasks=6, max_opt=S, horizon=H)
+    ts = [dict(r=0, d=int(rng.integers(0, H)), m=int(rng.integers(1, 30)), w=[3] * S, a0=100_000,
+               g=[10_000] * S) for _ in range(a)]
+    batch = gen.concat([batch_from_tasks(ts, S), tiny], S)
+    ocfg = OracleConfig(delta_micro=100_000, max_tasks=a, max_horizon=H)
+    ref = oracle.solve(batch, ocfg, TIME)
+    got = gpu_solve(batch, max_tasks=a, max_opt=S, max_horizon=H, delta=100_000)
+    assert_parity(got, ref, f"envelope S={S} H={H} N={a}")
