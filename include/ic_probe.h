@@ -12,10 +12,11 @@
  *   mode 1  LDS.128 + IADD         (the crossbar with a quarter of the instructions)
  *   mode 2  LDS.32 + VIADDMNMX     (the sweep's inner op: one option evaluation per lane)
  *
- * ic_probe_smem(device, mode, target_ms, &bytes_per_s, &bytes_per_clk_per_sm)
+ * ic_probe_smem(device, mode, target_ms, &bytes_per_s, &bytes_per_clk_per_sm, &sm_clock_hz)
  *   device: CUDA ordinal; target_ms: approximate kernel duration (1..1000).
- *   Outputs: achieved shared-memory load bytes / s over the whole GPU, and bytes per SM
- *   clock per SM.  Returns 0, -1 on invalid arguments, -3 on a CUDA error.  Synchronous;
+ *   Outputs: achieved shared-memory load bytes / s over the whole GPU (CUDA events), the SM
+ *   clock the probe ran at (SM cycles over the %globaltimer nanoseconds of the same window)
+ *   and the bytes per SM clock per SM that follow from the two.  Returns 0, -1 on invalid arguments, -3 on a CUDA error.  Synchronous;
  *   uses the legacy default stream of `device`.  Allocates and frees its own buffers.
  */
 #ifndef IC_PROBE_H
@@ -25,7 +26,7 @@
 extern "C" {
 #endif
 int ic_probe_smem(int32_t device, int32_t mode, double target_ms, double* bytes_per_s,
-                  double* bytes_per_clk_per_sm);
+                  double* bytes_per_clk_per_sm, double* sm_clock_hz);
 #ifdef __cplusplus
 }
 #endif

@@ -149,11 +149,12 @@ PROBE_MODES = {"lds32": 0, "lds128": 1, "lds32_viaddmax": 2}
 def probe_smem(device: int = 0, mode: str = "lds32", target_ms: float = 50.0) -> dict:
     """ic_probe_smem (include/ic_probe.h): measured shared-memory load bandwidth of `device`."""
     lib = load_library()
-    bps, bpc = ctypes.c_double(), ctypes.c_double()
-    rc = lib.ic_probe_smem(device, PROBE_MODES[mode], target_ms, ctypes.byref(bps), ctypes.byref(bpc))
+    bps, bpc, clk = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    rc = lib.ic_probe_smem(device, PROBE_MODES[mode], target_ms, ctypes.byref(bps), ctypes.byref(bpc),
+                           ctypes.byref(clk))
     if rc != 0:
         raise ICSchedError("ic_probe_smem", rc)
-    return {"mode": mode, "gbs": bps.value / 1e9, "bytes_per_clk_per_sm": bpc.value}
+    return {"mode": mode, "gbs": bps.value / 1e9, "bytes_per_clk_per_sm": bpc.value, "sm_mhz": clk.value / 1e6}
 
 
 _lib = None
@@ -197,7 +198,7 @@ def load_library():
         lib.ic_sched_state_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         lib.ic_sim_run.argtypes = [P(SimConfig), P(SimResult)]
         lib.ic_probe_smem.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P(ctypes.c_double),
-                                      P(ctypes.c_double)]
+                                      P(ctypes.c_double), P(ctypes.c_double)]
         for f in EXPORTED:
             getattr(lib, f).restype = ctypes.c_int
         lib.ic_sched_state_bytes.restype = ctypes.c_int64

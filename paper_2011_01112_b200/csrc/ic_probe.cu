@@ -12,9 +12,13 @@ constexpr int kThreads = 1024, kWords = 9216;  // 36 KB of shared memory per CTA
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 2) smem_probe(int iters, int key, int* sink,
                                                             long long* cycles) {
+  // cycles[blockIdx.x] = SM cycles of this CTA's timed loop; CTA 0 also records the
+  // global nanosecond timer over the same window (cycles[gridDim.x]) -> the SM clock it ran at
   __shared__ __align__(16) int buf[kWords];
   for (int i = threadIdx.x; i < kWords; i += kThreads) buf[i] = i * 2654435761u;
   __syncthreads();
+  unsigned long long g0 = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   const long long t0 = clock64();
   int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (MODE == 1) {
@@ -37,6 +41,11 @@ __global__ void __launch_bounds__(kThreads, 2) smem_probe(int iters, int key, in
   }
   __syncthreads();
   const long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    cycles[gridDim.x] = (long long)(g1 - g0);
+  }
   int s = 0;
 #pragma unroll
   for (int u = 0; u < 8; ++u) s ^= acc[u];
@@ -45,7 +54,7 @@ __global__ void __launch_bounds__(kThreads, 2) smem_probe(int iters, int key, in
 }
 
 template <int MODE>
-int run(int sms, int iters, float* ms, double* cyc_mean, int* sink, long long* cycles) {
+int run(int sms, int iters, float* ms, double* cyc_mean, double* clk_hz, int* sink, long long* cycles) {
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -3;
   const int grid = 2 * sms;
@@ -57,9 +66,10 @@ int run(int sms, int iters, float* ms, double* cyc_mean, int* sink, long long* c
   cudaEventElapsedTime(ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  long long h[2 * 1024];
-  if (grid > 2 * 1024 || cudaMemcpy(h, cycles, sizeof(long long) * grid, cudaMemcpyDeviceToHost) != cudaSuccess)
+  long long h[2 * 1024 + 1];
+  if (grid > 2 * 1024 || cudaMemcpy(h, cycles, sizeof(long long) * (grid + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
     return -3;
+  *clk_hz = h[grid] > 0 ? (double)h[0] / (h[grid] * 1e-9) : 0.0;
   double c = 0;
   for (int i = 0; i < grid; ++i) c += (double)h[i];
   *cyc_mean = c / grid;
@@ -69,8 +79,9 @@ int run(int sms, int iters, float* ms, double* cyc_mean, int* sink, long long* c
 }  // namespace
 
 extern "C" int ic_probe_smem(int32_t device, int32_t mode, double target_ms, double* bytes_per_s,
-                             double* bytes_per_clk_per_sm) {
-  if (mode < 0 || mode > 2 || !bytes_per_s || !bytes_per_clk_per_sm || !(target_ms >= 1 && target_ms <= 1000))
+                             double* bytes_per_clk_per_sm, double* sm_clock_hz) {
+  if (mode < 0 || mode > 2 || !bytes_per_s || !bytes_per_clk_per_sm || !sm_clock_hz ||
+      !(target_ms >= 1 && target_ms <= 1000))
     return -1;
   if (cudaSetDevice(device) != cudaSuccess) return -3;
   int sms = 0;
@@ -78,13 +89,15 @@ extern "C" int ic_probe_smem(int32_t device, int32_t mode, double target_ms, dou
   int* sink = nullptr;
   long long* cycles = nullptr;
   if (cudaMalloc(&sink, 4) != cudaSuccess) return -3;
-  if (cudaMalloc(&cycles, sizeof(long long) * 2 * sms) != cudaSuccess) {
+  if (cudaMalloc(&cycles, sizeof(long long) * (2 * sms + 1)) != cudaSuccess) {
     cudaFree(sink);
     return -3;
   }
+  double clk = 0;
   auto go = [&](int iters, float* ms, double* cyc) {
-    return mode == 0 ? run<0>(sms, iters, ms, cyc, sink, cycles)
-                     : mode == 1 ? run<1>(sms, iters, ms, cyc, sink, cycles) : run<2>(sms, iters, ms, cyc, sink, cycles);
+    return mode == 0   ? run<0>(sms, iters, ms, cyc, &clk, sink, cycles)
+           : mode == 1 ? run<1>(sms, iters, ms, cyc, &clk, sink, cycles)
+                       : run<2>(sms, iters, ms, cyc, &clk, sink, cycles);
   };
   // calibrate the iteration count to about target_ms, then measure
   int iters = 256, rc = 0;
@@ -101,7 +114,10 @@ extern "C" int ic_probe_smem(int32_t device, int32_t mode, double target_ms, dou
     const double per_thread = (mode == 1 ? 16.0 : 4.0) * 8.0 * iters;
     const double bytes_cta = per_thread * kThreads;
     *bytes_per_s = bytes_cta * 2.0 * sms / (ms * 1e-3);
-    *bytes_per_clk_per_sm = 2.0 * bytes_cta / cyc;  // two resident CTAs share one SM's crossbar
+    *sm_clock_hz = clk;
+    // per SM clock: the event-timed rate over the clock the SMs ran at (CTA 0's cycles over
+    // the global timer); the mean CTA cycle count is the cross-check (two CTAs share an SM)
+    *bytes_per_clk_per_sm = clk > 0 ? *bytes_per_s / (sms * clk) : 2.0 * bytes_cta / cyc;
   }
   cudaFree(sink);
   cudaFree(cycles);

@@ -7,6 +7,7 @@
 
 #include "../../include/ic_sched.h"
 #include "ic_sched_kernel.cuh"
+#include "ic_solo_kernel.cuh"
 
 using icsched::Params;
 
@@ -79,6 +80,44 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
   return L;
 }
 
+// One warp's private region in the solo kernel (ic_solo_kernel.cuh): a single in-place row
+// and one slot of the per-task tables.  Offsets are relative to the warp's base.
+Layout make_solo_layout(const ic_sched_config& c, int pad) {
+  Layout L{};
+  const int cols = (c.max_horizon + 31) / 32;
+  const int cap = 32 * cols;
+  const int mt = c.max_tasks;
+  L.nq = (cols + 7) / 8;
+  L.kp = (c.max_opt_stages + 2) & ~1;
+  L.r1 = c.max_opt_stages + 1;
+  int np2 = 1;
+  while (np2 < mt) np2 <<= 1;
+  L.np2 = np2 < 32 ? 32 : np2;
+  L.pad = pad;
+  L.rs = (pad + cap + 3) & ~3;
+  L.nbuf = 1;
+  L.nslots = 1;
+  L.ndec = 1;
+  int o = 0;
+  L.off_rowbuf = o; o = align16(o + L.rs * 4);
+  L.off_dec = o;
+  L.off_rowp = o;   o = align16(o + (mt * L.kp + 8) * 8);
+  L.off_info = o;   o = align16(o + mt * 16);
+  L.off_task = o;   o = align16(o + mt * 4);
+  L.off_tail = o;
+  L.off_misc = o;   o = align16(o + 16 * 8);
+  L.off_chosen = o; o = align16(o + mt * 4);
+  L.off_sd = o;     o = align16(o + mt * 4);
+  L.off_sr = o;     o = align16(o + mt * 4);
+  L.off_sS = o;     o = align16(o + mt * 4);
+  L.off_key = o;    o = align16(o + L.np2 * 8);
+  L.off_aux = o;    o = align16(o + mt * 4);
+  L.off_sQ = o;     o = align16(o + mt * 4);
+  L.cap = cap;
+  L.bytes = o;  // per warp
+  return L;
+}
+
 }  // namespace
 
 struct ic_sched {
@@ -99,6 +138,13 @@ struct ic_sched {
   cudaEvent_t ev[3 * 4 + 2];
   int64_t* tb_pinned;  // [3][chunk+1] rebased CSR offsets of the staged chunks
   int64_t tb_cap;
+  // solo kernel (one warp per instance) for plain solves when chosen; the state / re-plan
+  // entry points always use the warp-specialised kernel above
+  KernelFn solo_fn;
+  Layout SL;
+  int solo_grid, solo_ctas_per_sm;
+  uint32_t* solo_dec;
+  int64_t solo_dec_warp_words;
   int axis_mode;       // tuning, fixed at create: 0 auto per instance, 1 time, 2 reward
   int ckpt;            // re-plan checkpoint spacing (rows), power of two
   int no_vec_loads;    // 1: scalar descriptor loads only
@@ -234,6 +280,39 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
       return IC_ERR_OOM;
     }
   }
+  // one warp per instance for one-warp rows (H <= 1024) unless the warp-specialised kernel
+  // is asked for (tuning.kernel = 1); tuning.kernel = 2 forces it at any horizon
+  const bool ws_knobs = tu.dp_warps || tu.in_place || tu.slots || tu.decisions || tu.option_tables;
+  const bool solo = tu.kernel == 2 || (tu.kernel == 0 && !ws_knobs && nw == 1 && !sb);
+  if (solo) {
+    int rc = IC_OK;
+    const int spad = tu.pad_cols ? ((tu.pad_cols + 31) & ~31) : 64 > c.max_horizon ? ((c.max_horizon + 31) & ~31) : 64;
+    Layout S = make_solo_layout(c, spad);
+    KernelFn sf = icsched::kernel_solo(drop);
+    const int bytes = S.bytes * IC_SOLO_WPC;
+    int sp = 0;
+    if (bytes > kSmemLimit) rc = IC_ERR_LIMIT;
+    if (rc == IC_OK && cudaFuncSetAttribute(sf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) != cudaSuccess)
+      rc = IC_ERR_CUDA;
+    if (rc == IC_OK &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sp, sf, 32 * IC_SOLO_WPC, bytes) != cudaSuccess)
+      rc = IC_ERR_CUDA;
+    if (rc == IC_OK && sp < 1) rc = IC_ERR_LIMIT;
+    if (rc == IC_OK && tu.ctas_per_sm && tu.ctas_per_sm < sp) sp = tu.ctas_per_sm;
+    if (rc == IC_OK) {
+      h->solo_fn = sf;
+      h->SL = S;
+      h->solo_ctas_per_sm = sp;
+      h->solo_grid = sms * sp;
+      h->solo_dec_warp_words = (int64_t)c.max_tasks * S.nq * 32;
+      if (cudaMalloc(&h->solo_dec, (size_t)h->solo_dec_warp_words * 4 * h->solo_grid * IC_SOLO_WPC) != cudaSuccess)
+        rc = IC_ERR_OOM;
+    }
+    if (rc != IC_OK) {
+      ic_sched_destroy(h);
+      return rc;
+    }
+  }
   *out = h;
   return IC_OK;
 }
@@ -243,6 +322,7 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
   cudaSetDevice(h->cfg.device);
   if (h->dec_global) cudaFree(h->dec_global);
   if (h->rowp_g) cudaFree(h->rowp_g);
+  if (h->solo_dec) cudaFree(h->solo_dec);
   if (h->work) cudaFree(h->work);
   if (h->stage) cudaFree(h->stage);
   if (h->s_in) {
@@ -258,6 +338,18 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
 
 extern "C" int ic_sched_get_info(const ic_sched* h, ic_sched_info* info) {
   if (!h || !info) return IC_ERR_INVALID_ARG;
+  if (h->solo_fn) {  // plain solves run one warp per instance
+    info->threads_per_cta = 32 * IC_SOLO_WPC;
+    info->cols_per_thread = (h->cfg.max_horizon + 31) / 32;
+    info->ctas_per_sm = h->solo_ctas_per_sm;
+    info->grid = h->solo_grid;
+    info->smem_bytes = h->SL.bytes * IC_SOLO_WPC;
+    info->decisions_in_smem = 0;
+    info->double_buffered = 0;
+    info->pad_cols = h->SL.pad;
+    info->workspace_bytes = h->solo_dec_warp_words * 4 * h->solo_grid * IC_SOLO_WPC;
+    return IC_OK;
+  }
   info->threads_per_cta = 32 * (h->nw + 1);
   info->cols_per_thread = (h->cfg.max_horizon + 32 * h->nw - 1) / (32 * h->nw);
   info->ctas_per_sm = h->ctas_per_sm;
@@ -395,6 +487,41 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.rowp_slab = h->rowp_slab;
   p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
                ((uintptr_t)p.opt_gain & 15) == 0 && !h->no_vec_loads;
+  if (h->solo_fn && !state) {  // one warp per instance (ic_solo_kernel.cuh)
+    const Layout& S = h->SL;
+    p.pad = S.pad;
+    p.nq = S.nq;
+    p.np2 = S.np2;
+    p.dec_smem = 0;
+    p.dec_global = h->solo_dec;
+    p.dec_slab_words = h->solo_dec_warp_words;
+    p.dec_words = h->solo_dec_warp_words;
+    p.ndec = 1;
+    p.nslots = 1;
+    p.cap = S.cap;
+    p.rowbuf_stride = S.rs;
+    p.solo_warp_bytes = S.bytes;
+    p.off_rowbuf = S.off_rowbuf;
+    p.off_dec = S.off_dec;
+    p.off_rowp = S.off_rowp;
+    p.off_info = S.off_info;
+    p.off_task = S.off_task;
+    p.off_tail = S.off_tail;
+    p.off_misc = S.off_misc;
+    p.off_chosen = S.off_chosen;
+    p.off_sd = S.off_sd;
+    p.off_sr = S.off_sr;
+    p.off_sS = S.off_sS;
+    p.off_key = S.off_key;
+    p.off_aux = S.off_aux;
+    p.off_sQ = S.off_sQ;
+    p.rowp_g = nullptr;
+    int64_t grid = h->solo_grid;
+    const int64_t need = (in->n_instances + IC_SOLO_WPC - 1) / IC_SOLO_WPC;
+    if (grid > need) grid = need;
+    h->solo_fn<<<(unsigned)grid, 32 * IC_SOLO_WPC, S.bytes * IC_SOLO_WPC, (cudaStream_t)cuda_stream>>>(p);
+    return cudaGetLastError() == cudaSuccess ? IC_OK : IC_ERR_CUDA;
+  }
   int64_t grid = h->grid;
   if (grid > in->n_instances) grid = in->n_instances;
   h->fn<<<(unsigned)grid, 32 * (h->nw + 1), h->L.bytes, (cudaStream_t)cuda_stream>>>(p);

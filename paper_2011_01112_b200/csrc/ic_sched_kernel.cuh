@@ -79,6 +79,7 @@ struct Params {
   int nslots;  // 2: set up instance b+1 while the DP sweeps b; 1: serialised (large N)
   int cap;     // row buffer capacity in columns (32 NW x COLS)
   int off_aux, off_sQ;
+  int solo_warp_bytes;  // solo kernel: shared-memory bytes of one warp's private region
   int axis_mode;  // 0 auto (per instance), 1 time axis only, 2 reward axis whenever eligible
   // NEXT-2 (incremental re-plan): per-instance state = every DP row (its active
   // columns and tail value, stride H+1), the decisions and the tail nibbles
@@ -224,6 +225,58 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     if (gcl > 0)  // rare: options longer than the pad
       for (; g0 < ng && g0 < gcl; g0 += 8) chunk(g0, std::true_type{});
     for (; g0 < ng; g0 += 8) chunk(g0, std::false_type{});
+  } else if constexpr (NW == 1) {
+    // one warp per instance (the solo kernel), in place from high to low columns: blocks of
+    // NB consecutive groups, each loads -> __syncwarp -> stores.  A block reads only columns
+    // below its top, so its stores cannot disturb a lower block still to be computed.  The
+    // ragged top chunk goes first as blocks of 1, 2 and 4 groups (highest first), then full
+    // chunks of 8 groups (two blocks of 4 when K is large, to bound the values in flight).
+    auto blk = [&](int g, auto nb_tag, auto clamp_tag) -> uint32_t {
+      constexpr int NB = decltype(nb_tag)::value;
+      const int tb = g * NT + tid;
+      int v[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) v[u] = cell(tb + u * NT, clamp_tag);
+      __syncwarp();
+      uint32_t dw = 0;
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        dw |= (uint32_t)(v[u] & 15) << (4 * (u + (g & 7)));
+        nxt[tb + u * NT] = stv(v[u]);
+      }
+      return dw;
+    };
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I4 = std::integral_constant<int, 4>;
+    using I8 = std::integral_constant<int, 8>;
+    const int gtop = ng & ~7, rem = ng - gtop;
+    if (rem) {
+      auto ragged = [&](auto clamp_tag) {
+        uint32_t dw = 0;
+        if (rem & 1) dw |= blk(gtop + (rem & 6), I1{}, clamp_tag);
+        if (rem & 2) dw |= blk(gtop + (rem & 4), I2{}, clamp_tag);
+        if (rem & 4) dw |= blk(gtop, I4{}, clamp_tag);
+        decrow[(gtop >> 3) * NT + tid] = dw;
+      };
+      if (gtop < gcl)
+        ragged(std::true_type{});
+      else
+        ragged(std::false_type{});
+    }
+    auto full = [&](int g0, auto clamp_tag) {
+      uint32_t dw;
+      if constexpr (KK <= IC_BATCH_KSPLIT) {
+        dw = blk(g0, I8{}, clamp_tag);
+      } else {
+        dw = blk(g0 + 4, I4{}, clamp_tag);
+        dw |= blk(g0, I4{}, clamp_tag);
+      }
+      decrow[(g0 >> 3) * NT + tid] = dw;
+    };
+    int g0 = gtop - 8;
+    for (; g0 >= 0 && g0 >= gcl; g0 -= 8) full(g0, std::false_type{});
+    for (; g0 >= 0; g0 -= 8) full(g0, std::true_type{});  // rare: options longer than the pad
   } else {
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
     // chunk c reads only columns below its top, so writing it after the barrier
@@ -590,7 +643,10 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
 }
 
 // a6: backtrack from (Q*, t*) through the decision nibbles (one lane).
-template <int NW>
+// SOLO: the solo kernel keeps no tail nibbles; a column past a row's deadline takes the
+// decision of the deadline column itself (every G_i(t), t > d_i, equals G_i(d_i) with the
+// same argmax: the options read G_{i-1}(d_i - C_k) and the drop reads M_{i-1} there).
+template <int NW, bool SOLO = false>
 __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, int s, int lane, int db) {
   constexpr int NT = 32 * NW;
   const long long* mi = S.misc + s * 16;
@@ -613,7 +669,14 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
       return rw ? tt - sh : min(tt, inf[pos].x) - sh;
     };
     auto nibble = [&](int row, int tt) -> int {
-      if (!rw && tt > inf[row].x) return tailn[row];  // past the deadline: the row's tail nibble
+      if (!rw && tt > inf[row].x) {  // past the deadline
+        if constexpr (SOLO) {
+          if (inf[row].x < 0) return 15;  // no active column: the task is dropped
+          tt = inf[row].x;
+        } else {
+          return tailn[row];  // the row's tail nibble
+        }
+      }
       const int g = tt / NT, l = tt - g * NT;
       const uint32_t w = dbase[((size_t)row * p.nq + (g >> 3)) * NT + l];
       return (int)((w >> (4 * (g & 7))) & 15u);

@@ -1,0 +1,173 @@
+// ic_solo_kernel.cuh — one warp per instance, for short rows (H <= 1024: C1, C2).
+//
+// The warp-specialised kernel (ic_sched_kernel.cuh) pairs every sweep with a tail warp
+// that sets up instance b+1 and backtracks b.  When a row is one warp wide that pairing
+// costs half of the SM's warp slots and registers for a warp that idles two thirds of
+// the time, and it lands the DP warps and the tail warps on different SM sub-partitions
+// (ncu, profiles/r01_ncu_C2_summary.json: 33 % of all stall samples are idle tail warps).
+// Here every warp runs the whole path a1-a8 for its own instances, one after another:
+//
+//   a1-a3  tail_setup (descriptor loads, prefix sums, Delta, packed keys, EDF sort)
+//   a4     the time-indexed dual of Eqs. 1-2 or the paper's reward-indexed
+//          table, one row at a time IN PLACE (a single row buffer: chunks from high to
+//          low columns, loads -> __syncwarp -> stores, dp_row<1, true, ...>), so a warp
+//          needs only (pad + H) * 4 bytes of shared memory for its row;
+//   a5     Q* = G_N(T) and the least t* (32-ary ballot search), or r* on the reward axis;
+//   a6-a8  tail_backtrack<1, true> / tail_outputs, as in the other kernel.
+//
+// Tail collapse without tail codes: after row i's sweep, the cell at column d_i already
+// holds M_i = max(M_{i-1}, A_i) (the drop term reads G_{i-1}(d_i) = M_{i-1}), so the
+// warp reads it back, fills (d_i, d_{i+1}] with it, and the backtrack reads the decision
+// at min(t, d_i).  Latency of one warp's dependent steps (setup loads, backtrack chain)
+// is hidden by the other resident warps instead of by warp specialisation.
+#pragma once
+#include "ic_sched_kernel.cuh"
+
+#ifndef IC_SOLO_WPC
+#define IC_SOLO_WPC 4  // warps per CTA (independent instances; a CTA is only a packing unit)
+#endif
+#ifndef IC_SOLO_MINB
+#define IC_SOLO_MINB 7  // CTAs per SM the register budget is sized for (28 warps)
+#endif
+
+namespace icsched {
+
+template <bool DROP>
+__global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel(const Params p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* base = smem + (size_t)warp * p.solo_warp_bytes;
+  Smem S;
+  S.rowbuf = (int32_t*)(base + p.off_rowbuf);
+  S.dec = p.dec_global + ((int64_t)blockIdx.x * IC_SOLO_WPC + warp) * p.dec_slab_words;
+  S.rowp = (int2*)(base + p.off_rowp);
+  S.info = (int4*)(base + p.off_info);
+  S.task = (int32_t*)(base + p.off_task);
+  S.tail = nullptr;
+  S.misc = (long long*)(base + p.off_misc);
+  S.chosen = (int32_t*)(base + p.off_chosen);
+  S.sd = (int32_t*)(base + p.off_sd);
+  S.sr = (int32_t*)(base + p.off_sr);
+  S.sS = (int32_t*)(base + p.off_sS);
+  S.key = (unsigned long long*)(base + p.off_key);
+  S.aux = (int32_t*)(base + p.off_aux);
+  S.sQ = (int32_t*)(base + p.off_sQ);
+  int32_t* const buf = S.rowbuf + p.pad;
+  int padmode = -1;  // value in the pad cells: 0 NEG (time axis), 1 INFV (reward axis)
+  unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const size_t dec_row_words = (size_t)p.nq * 32;
+  const int kp = p.kp;
+
+  for (;;) {
+    // ---- a1-a3: claim an instance and set it up (instances the DP never sees are written here)
+    int64_t b;
+    do {
+      unsigned long long v = 0;
+      if (lane == 0) v = atomicAdd(&p.work[0], 1ull);
+      b = (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    } while (b < p.B && tail_setup<1>(p, S, b, 0, lane, acc) != ST_OK);
+    if (b >= p.B) break;
+    long long* mi = S.misc;
+    const int n = (int)mi[0];
+    const bool rw = mi[9] != 0;
+    const int d_first = (int)mi[7], dl = (int)mi[8];
+    if ((int)rw != padmode) {  // the pad left of column 0 reads as "invalid" on this axis
+      padmode = rw;
+      for (int i = lane; i < p.pad; i += 32) S.rowbuf[i] = rw ? INFV : NEG;
+    }
+    if (rw) {  // P(0, 0) = 0, P(0, r > 0) = infinity over every column the instance reaches
+      for (int t = lane; t <= dl; t += 32) buf[t] = t == 0 ? 0 : INFV;
+    } else {
+      for (int t = lane; t <= d_first; t += 32) buf[t] = 15;  // G_0(t) = 0
+    }
+    __syncwarp();
+    // ---- a4: the rows, in place
+    const int4* inf = S.info;
+    const int2* ops = S.rowp;
+    uint32_t* decrow = S.dec;
+    int M = 15;
+#pragma unroll 1
+    for (int pos = 0; pos < n; ++pos) {
+      const int4 f = inf[pos];
+      const int d = f.x, K = f.y & 255;
+      if (rw) {
+        // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
+        dp_row_dispatch<1, true, DROP, true>(K, false, buf, buf, decrow, (const int4*)ops, d, 0, p.pad,
+                                             S.aux[pos]);
+        __syncwarp();
+      } else {
+        const bool gen = (f.y >> 8) & 1;
+        dp_row_dispatch<1, true, DROP, false>(K, gen, buf, buf, decrow, (const int4*)ops, d, f.z, p.pad, 0);
+        __syncwarp();
+        // M_pos = G_pos(d) (tail collapse); G_pos(t) = M_pos on (d, d_next] for the next row
+        if (d >= 0)
+          M = buf[d];
+        else if (!DROP)
+          M = NEG | 15;
+        const int dn = f.w;
+        if (dn > d) {
+          const int first = d + 1 > 0 ? d + 1 : 0;
+          for (int t = first + lane; t <= dn; t += 32) buf[t] = M;
+        }
+        __syncwarp();
+      }
+      ops += kp;
+      decrow += dec_row_words;
+    }
+    // ---- a5: the optimum of row N
+    if (rw) {  // r* = the largest finite column (reading R6)
+      int best = -1;
+      for (int t = lane; t <= dl; t += 32)
+        if (buf[t] < INFV) best = t;
+      best = __reduce_max_sync(0xffffffffu, best);
+      if (lane == 0) {
+        mi[5] = best;
+        mi[6] = best;
+      }
+    } else {  // Q* = G_N(T), t* = least t with G_N(t) = Q* (G_N non-decreasing on [0, d_N])
+      long long Qv, ts = 0;
+      if (dl < 0) {
+        Qv = M;
+      } else {
+        Qv = buf[dl];
+        int lo = 0, hi = dl;
+        while (lo < hi) {
+          const int step = (hi - lo + 32) / 32;
+          int x = lo + (lane + 1) * step - 1;
+          if (x > hi) x = hi;
+          const unsigned m = __ballot_sync(0xffffffffu, buf[x] >= Qv);
+          const int fl = __ffs(m) - 1;
+          const int nhi = fl == 0 ? min(lo + step - 1, hi) : min(lo + (fl + 1) * step - 1, hi);
+          const int nlo = fl == 0 ? lo : lo + fl * step;
+          lo = nlo;
+          hi = nhi;
+        }
+        ts = lo;
+      }
+      if (lane == 0) {
+        mi[5] = Qv >= 0 ? (Qv >> 4) : -1;
+        mi[6] = ts;
+      }
+    }
+    __syncwarp();
+    // ---- a6-a8
+    tail_backtrack<1, true>(p, S, 0, lane, 0);
+    tail_outputs<1>(p, S, 0, lane, acc);
+  }
+  if (lane == 0 && p.stats) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (acc[i]) atomicAdd(&p.stats[i], acc[i]);
+  }
+  if (lane == 0) {  // the last warp out resets the counters for the next launch
+    __threadfence();
+    if (atomicAdd(&p.work[1], 1ull) == (unsigned long long)gridDim.x * IC_SOLO_WPC - 1) {
+      p.work[0] = 0;
+      p.work[1] = 0;
+    }
+  }
+}
+
+KernelFn kernel_solo(bool drop);
+
+}  // namespace icsched

@@ -73,7 +73,10 @@ def _check_sample(cw, inputs, out, starts, run):
     rows = (ids[:, None] * N + torch.arange(N, device="cuda")[None, :]).reshape(-1)
     # the oracle's instances are the ones the GPU solved (same generator, built twice)
     for f in ("release", "deadline", "mand_wcet", "n_opt", "mand_conf", "opt_wcet", "opt_gain"):
-        np.testing.assert_array_equal(inputs[f][rows].cpu().numpy(), getattr(host, f), err_msg=f)
+        x = inputs[f]
+        x = x.view(torch.int32) if x.dtype == torch.uint32 else x  # no uint32 gather on CUDA
+        h = getattr(host, f)
+        np.testing.assert_array_equal(x[rows].cpu().numpy().view(h.dtype), h, err_msg=f)
     ocfg = OracleConfig(epsilon_micro=cw.epsilon_micro, max_tasks=N, max_horizon=cw.horizon)
     ref = oracle.solve(host, ocfg, TIME)
     got = {k: (out[k][rows] if k in ("kept", "start", "finish") else out[k][ids]).cpu().numpy()

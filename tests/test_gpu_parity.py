@@ -179,7 +179,8 @@ def test_decision_placement(decisions):
     assert_parity(got, ref, f"decisions={decisions}")
 
 
-@pytest.mark.parametrize("tuning", [dict(dp_warps=1), dict(dp_warps=2), dict(dp_warps=4), dict(dp_warps=8),
+@pytest.mark.parametrize("tuning", [dict(dp_warps=1, kernel=1), dict(kernel=2), dict(kernel=2, pad_cols=32),
+                                    dict(kernel=2, axis=1), dict(dp_warps=2), dict(dp_warps=4), dict(dp_warps=8),
                                     dict(dp_warps=16), dict(in_place=1, dp_warps=8), dict(in_place=1, dp_warps=16),
                                     dict(pad_cols=32), dict(slots=1, dp_warps=2),
                                     dict(slots=1, in_place=1, dp_warps=8), dict(option_tables=1, dp_warps=8),
@@ -377,3 +378,23 @@ def test_create_envelope(S, H, lo, hi):
     ref = oracle.solve(batch, ocfg, TIME)
     got = gpu_solve(batch, max_tasks=a, max_opt=S, max_horizon=H, delta=100_000)
     assert_parity(got, ref, f"envelope S={S} H={H} N={a}")
+
+
+@pytest.mark.parametrize("name,n", [("C1", 4000), ("C2", 1500)])
+@pytest.mark.parametrize("delta", [0, 100_000])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_solo_and_warp_specialised_kernels_agree(name, n, delta, mode):
+    """The one-warp-per-instance kernel (default for H <= 1024) and the warp-specialised kernel
+    (tuning kernel=1) both equal the oracle on the same batch, both sweep axes, releases."""
+    cw = gen.CONFIGS[name]
+    rng = np.random.default_rng(90 + mode)
+    rel = gen.tiny_random(rng, 300, max_tasks=cw.n_tasks, max_opt=cw.n_opt, horizon=cw.horizon, p_release=0.7)
+    batch = gen.concat([gen.generate(cw, n), rel], cw.n_opt)
+    ocfg = OracleConfig(drop_mode=mode, delta_micro=delta, epsilon_micro=cw.epsilon_micro, max_tasks=cw.n_tasks,
+                        max_horizon=cw.horizon)
+    ref = oracle.solve(batch, ocfg, TIME)
+    for kernel in (0, 1, 2):
+        got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
+                        delta=delta, eps=cw.epsilon_micro, tuning=dict(kernel=kernel))
+        assert_parity(got, ref, f"{name} kernel={kernel} delta={delta} mode={mode}")
+        assert (got["_info"]["threads_per_cta"] == 128) == (kernel != 1)
