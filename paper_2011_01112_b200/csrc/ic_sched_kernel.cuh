@@ -128,7 +128,9 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
                                        const int r, const int kr, const int pad, const int lim) {
   constexpr int NT = 32 * NW;
   constexpr int KK = GEN ? KMAX : K;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  // one-warp rows are swept by warp 0 of the warp-specialised kernel or by any warp of the
+  // solo kernel: the lane is the thread's column offset there
+  const int tid = NW == 1 ? (int)(threadIdx.x & 31) : (int)threadIdx.x, warp = NW == 1 ? 0 : tid >> 5;
   int C[KK > 0 ? KK : 1], key[KK > 0 ? KK : 1];
 #pragma unroll
   for (int k = 0; k < KK; k += 2) {
