@@ -105,7 +105,7 @@ Layout make_solo_layout(const ic_sched_config& c, int pad) {
   L.off_info = o;   o = align16(o + mt * 16);
   L.off_task = o;   o = align16(o + mt * 4);
   L.off_tail = o;
-  L.off_misc = o;   o = align16(o + 16 * 8);
+  L.off_misc = o;   o = align16(o + 24 * 8);  // [0..15] instance header, [16..23] stats
   L.off_chosen = o; o = align16(o + mt * 4);
   L.off_sd = o;     o = align16(o + mt * 4);
   L.off_sr = o;     o = align16(o + mt * 4);

@@ -115,8 +115,10 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
 
 // ---------------------------------------------------------------------------
-// DP warps: one row, active columns t <= d.  K options (compile-time; GEN =
-// general path with runtime kr options and per-option release masks).
+// DP warps: one row, active columns t <= d.  K options (compile-time), or GEN = the
+// general path with runtime kr options, per-option release masks, and sources left of
+// the pad redirected to the pad cell at -1 (rows with releases, or whose longest option
+// reaches past the pad: the tail warp flags them, so the common rows carry no bounds code).
 // RW = the reward-indexed axis (NEXT-1, the paper's own Eqs. 1-2): a cell holds the
 // least finish time P(i, r)*16 of the first i EDF tasks reaching exactly quantised
 // reward r; option k shifts by q_k and adds C_k*16 + (k+1) (the code), so one
@@ -125,7 +127,7 @@ __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax
 template <int NW, bool SB, bool DROP, int K, bool GEN, bool RW>
 __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
                                        const int4* __restrict__ ops4, const int4 (&pre)[4], const int d,
-                                       const int r, const int kr, const int pad, const int lim) {
+                                       const int r, const int kr, const int lim) {
   constexpr int NT = 32 * NW;
   constexpr int KK = GEN ? KMAX : K;
   // one-warp rows are swept by warp 0 of the warp-specialised kernel or by any warp of the
@@ -144,37 +146,26 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       }
     }
   }
-  int reachC = 0;
-  if (RW) {  // the tail warp stored the reward-axis form: shift q, add C*16 + k+1
-#pragma unroll
-    for (int k = 0; k < KK; ++k) reachC = max(reachC, C[k]);
-  } else if (KK > 0) {
-    reachC = C[KK - 1];
-  }
   const int w0 = warp * 32;
   const int ng = d >= w0 ? (d - w0) / NT + 1 : 0;  // this warp's groups holding a column t <= d
-  // groups whose longest option reaches left of the pad read through a clamp
-  const int reach = (!GEN && KK > 0) ? reachC - pad - w0 : 0;
-  const int gcl = GEN ? ng : (reach > 0 ? (reach + NT - 1) / NT : 0);
-  auto cell = [&](int t, auto clamp_tag) -> int {
-    constexpr bool CL = decltype(clamp_tag)::value;
+  auto cell = [&](int t) -> int {
     if constexpr (RW) {
       int a = INFV;
 #pragma unroll
-      for (int k = 0; k < KK; ++k) a = __viaddmin_s32(cur[CL ? max(t - C[k], -pad) : t - C[k]], key[k], a);
+      for (int k = 0; k < KK; ++k) {
+        if (!GEN || k < kr) a = __viaddmin_s32(cur[GEN ? max(t - C[k], -1) : t - C[k]], key[k], a);
+      }
       a = a <= lim ? a : INFV;
       return DROP ? min(cur[t], a) : a;
     } else {
       int v = DROP ? cur[t] : NEG;
 #pragma unroll
       for (int k = 0; k < KK; ++k) {
-        if (GEN) {  // releases: options with a source before r are invalid (read a NEG cell)
+        if (GEN) {  // sources before the release (or left of the pad) read the NEG pad cell at -1
           if (k < kr) {
             const int src = t - C[k];
             v = viaddmax(cur[src >= r ? src : -1], key[k], v);
           }
-        } else if (CL) {
-          v = viaddmax(cur[max(t - C[k], -pad)], key[k], v);
         } else {
           v = viaddmax(cur[t - C[k]], key[k], v);
         }
@@ -184,9 +175,9 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   };
   // stored value: time axis keeps low nibble 15 (the drop key), reward axis keeps it 0
   auto stv = [](int v) { return RW ? (v & ~15) : (v | 15); };
-  if (!SB) {
+  if constexpr (!SB) {
     constexpr int BATCH = (KK <= IC_BATCH_KSPLIT) ? 8 : IC_BATCH_HI;  // cells whose loads are in flight together
-    auto chunk = [&](int g0, auto clamp_tag) {
+    for (int g0 = 0; g0 < ng; g0 += 8) {
       const int tb = g0 * NT + tid;
       uint32_t dw = 0;
       if (g0 + 8 <= ng) {
@@ -194,7 +185,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         for (int h = 0; h < 8; h += BATCH) {
           int v[BATCH];
 #pragma unroll
-          for (int u = 0; u < BATCH; ++u) v[u] = cell(tb + (h + u) * NT, clamp_tag);
+          for (int u = 0; u < BATCH; ++u) v[u] = cell(tb + (h + u) * NT);
 #pragma unroll
           for (int u = 0; u < BATCH; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
@@ -209,7 +200,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
           constexpr int NB = decltype(nb_tag)::value;
           int v[NB];
 #pragma unroll
-          for (int u = 0; u < NB; ++u) v[u] = cell(tb + (u0 + u) * NT, clamp_tag);
+          for (int u = 0; u < NB; ++u) v[u] = cell(tb + (u0 + u) * NT);
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (u0 + u));
@@ -222,23 +213,19 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
       decrow[(g0 >> 3) * NT + tid] = dw;
-    };
-    int g0 = 0;
-    if (gcl > 0)  // rare: options longer than the pad
-      for (; g0 < ng && g0 < gcl; g0 += 8) chunk(g0, std::true_type{});
-    for (; g0 < ng; g0 += 8) chunk(g0, std::false_type{});
+    }
   } else if constexpr (NW == 1) {
     // one warp per instance (the solo kernel), in place from high to low columns: blocks of
     // NB consecutive groups, each loads -> __syncwarp -> stores.  A block reads only columns
     // below its top, so its stores cannot disturb a lower block still to be computed.  The
     // ragged top chunk goes first as blocks of 1, 2 and 4 groups (highest first), then full
     // chunks of 8 groups (two blocks of 4 when K is large, to bound the values in flight).
-    auto blk = [&](int g, auto nb_tag, auto clamp_tag) -> uint32_t {
+    auto blk = [&](int g, auto nb_tag) -> uint32_t {
       constexpr int NB = decltype(nb_tag)::value;
       const int tb = g * NT + tid;
       int v[NB];
 #pragma unroll
-      for (int u = 0; u < NB; ++u) v[u] = cell(tb + u * NT, clamp_tag);
+      for (int u = 0; u < NB; ++u) v[u] = cell(tb + u * NT);
       __syncwarp();
       uint32_t dw = 0;
 #pragma unroll
@@ -254,31 +241,23 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     using I8 = std::integral_constant<int, 8>;
     const int gtop = ng & ~7, rem = ng - gtop;
     if (rem) {
-      auto ragged = [&](auto clamp_tag) {
-        uint32_t dw = 0;
-        if (rem & 1) dw |= blk(gtop + (rem & 6), I1{}, clamp_tag);
-        if (rem & 2) dw |= blk(gtop + (rem & 4), I2{}, clamp_tag);
-        if (rem & 4) dw |= blk(gtop, I4{}, clamp_tag);
-        decrow[(gtop >> 3) * NT + tid] = dw;
-      };
-      if (gtop < gcl)
-        ragged(std::true_type{});
-      else
-        ragged(std::false_type{});
+      uint32_t dw = 0;
+      if (rem & 1) dw |= blk(gtop + (rem & 6), I1{});
+      if (rem & 2) dw |= blk(gtop + (rem & 4), I2{});
+      if (rem & 4) dw |= blk(gtop, I4{});
+      decrow[(gtop >> 3) * NT + tid] = dw;
     }
-    auto full = [&](int g0, auto clamp_tag) {
+#pragma unroll 1
+    for (int g0 = gtop - 8; g0 >= 0; g0 -= 8) {
       uint32_t dw;
       if constexpr (KK <= IC_BATCH_KSPLIT) {
-        dw = blk(g0, I8{}, clamp_tag);
+        dw = blk(g0, I8{});
       } else {
-        dw = blk(g0 + 4, I4{}, clamp_tag);
-        dw |= blk(g0, I4{}, clamp_tag);
+        dw = blk(g0 + 4, I4{});
+        dw |= blk(g0, I4{});
       }
       decrow[(g0 >> 3) * NT + tid] = dw;
-    };
-    int g0 = gtop - 8;
-    for (; g0 >= 0 && g0 >= gcl; g0 -= 8) full(g0, std::false_type{});
-    for (; g0 >= 0; g0 -= 8) full(g0, std::true_type{});  // rare: options longer than the pad
+    }
   } else {
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
     // chunk c reads only columns below its top, so writing it after the barrier
@@ -289,13 +268,8 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       const int g0 = c * CH;
       const int tb = g0 * NT + tid;
       int v[CH];
-      if (gcl > 0 && g0 < gcl) {  // rare: options longer than the pad
 #pragma unroll
-        for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::true_type{}) : 0;
-      } else {
-#pragma unroll
-        for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT, std::false_type{}) : 0;
-      }
+      for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT) : 0;
       bar_sync(BAR_DP, NT);
 #pragma unroll
       for (int w8 = 0; w8 < CH; w8 += 8) {
@@ -313,17 +287,17 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   }
 }
 
+// gen: the row takes the general path (releases, or an option longer than the pad).
 template <int NW, bool SB, bool DROP, bool RW>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
-                                                uint32_t* decrow, const int4* ops4, int d, int r, int pad,
-                                                int lim) {
+                                                uint32_t* decrow, const int4* ops4, int d, int r, int lim) {
   const int4 pre[4] = {ops4[0], ops4[1], ops4[2], ops4[3]};  // issued ahead of the K dispatch
-  if (!RW && gen) {
-    dp_row<NW, SB, DROP, KMAX, true, false>(cur, nxt, decrow, ops4, pre, d, r, K, pad, lim);
+  if (gen) {
+    dp_row<NW, SB, DROP, KMAX, true, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: dp_row<NW, SB, DROP, KK, false, RW>(cur, nxt, decrow, ops4, pre, d, r, K, pad, lim); break;
+  case KK: dp_row<NW, SB, DROP, KK, false, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -436,7 +410,7 @@ __device__ __forceinline__ void for_each_opt(const Params& p, int64_t t, int Sn,
 // prefix sums, q = R div Delta, packed keys, the row table of the DP.
 template <int NW>
 __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int lane,
-                          unsigned long long (&acc)[8]) {
+                          unsigned long long* acc) {
   const int64_t lo = p.task_begin[b];
   const int64_t n64 = p.task_begin[b + 1] - lo;
   if (n64 < 0 || n64 > p.max_tasks) {
@@ -564,10 +538,12 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
         R += g;
         option(k);
       });
-      const bool gen = r > 0;  // releases take the masked path; long options clamp per group
+      // the general path: releases, or (per axis) an option reaching past the pad
+      const bool gen = r > 0 || (K > 0 && rp[K - 1].x > p.pad);
+      const bool genr = qmax > p.pad;
       anyrel |= r > 0;
       const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
-      S.info[s * p.max_tasks + pos] = make_int4(d, K | (gen ? 256 : 0) | (Sn << 16), r, dn);
+      S.info[s * p.max_tasks + pos] = make_int4(d, K | (gen ? 256 : 0) | (genr ? 512 : 0) | (Sn << 16), r, dn);
       S.task[s * p.max_tasks + pos] = tk;
       S.aux[s * p.max_tasks + pos] = d * 16 + 15;
     }
@@ -725,7 +701,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
 // a7/a8: EDF schedule (warp max-plus scan), outputs in input order, stats.
 template <int NW>
 __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int s, int lane,
-                                             unsigned long long (&acc)[8]) {
+                                             unsigned long long* acc) {
   const long long* mi = S.misc + s * 16;
   const int n = (int)mi[0];
   const int64_t lo = mi[1], b = mi[2];
@@ -984,7 +960,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       int32_t* nxt = buf0 + ((pos + 1) & 1) * RSb;
       if (rw) {
         // reward axis: columns r <= Qpre_pos; (Qpre_pos, Qpre_next] are unreachable
-        dp_row_dispatch<NW, SB, DROP, true>(K, false, cur, nxt, decrow, (const int4*)ops, d, 0, p.pad,
+        dp_row_dispatch<NW, SB, DROP, true>(K, (f.y >> 9) & 1, cur, nxt, decrow, (const int4*)ops, d, 0,
                                             auxp[pos]);
         if (keep_state && ((pos + 1) & ckm) == 0) {  // checkpoint row for later re-plans
           int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
@@ -1001,7 +977,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         }
         int A = 0;
         if (SB) A = __reduce_max_sync(0xffffffffu, av);
-        dp_row_dispatch<NW, SB, DROP, false>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, p.pad, 0);
+        dp_row_dispatch<NW, SB, DROP, false>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, 0);
         if (!SB) A = __reduce_max_sync(0xffffffffu, av);
         const int Mv = DROP ? max(M, A) : A;
         if (tid == 0) tailp[pos] = Mv & 15;

@@ -32,14 +32,11 @@
 
 namespace icsched {
 
-template <bool DROP>
-__global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel(const Params p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* base = smem + (size_t)warp * p.solo_warp_bytes;
+// One warp's view of its private shared-memory region (offsets from make_solo_layout).
+__device__ __forceinline__ Smem solo_smem(const Params& p, unsigned char* base, uint32_t* dec) {
   Smem S;
   S.rowbuf = (int32_t*)(base + p.off_rowbuf);
-  S.dec = p.dec_global + ((int64_t)blockIdx.x * IC_SOLO_WPC + warp) * p.dec_slab_words;
+  S.dec = dec;
   S.rowp = (int2*)(base + p.off_rowp);
   S.info = (int4*)(base + p.off_info);
   S.task = (int32_t*)(base + p.off_task);
@@ -52,113 +49,140 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
   S.key = (unsigned long long*)(base + p.off_key);
   S.aux = (int32_t*)(base + p.off_aux);
   S.sQ = (int32_t*)(base + p.off_sQ);
-  int32_t* const buf = S.rowbuf + p.pad;
-  int padmode = -1;  // value in the pad cells: 0 NEG (time axis), 1 INFV (reward axis)
-  unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const size_t dec_row_words = (size_t)p.nq * 32;
-  const int kp = p.kp;
+  return S;
+}
+// the warp's statistics accumulators live in its misc block (slots 16..23), not in registers
+__device__ __forceinline__ unsigned long long* solo_acc(const Params& p, unsigned char* base) {
+  return (unsigned long long*)(base + p.off_misc) + 16;
+}
 
+// a1-a3 for instance b (tail_setup); ST_OK if the sweep must run.  The three phases are
+// separate (non-inlined) functions so that each gets the whole register budget: the
+// setup's sort keys and the sweep's option tables are never live at the same time.
+static __device__ __noinline__ int solo_setup(const Params& p, unsigned char* base, int64_t b, int lane) {
+  const Smem S = solo_smem(p, base, nullptr);
+  return tail_setup<1>(p, S, b, 0, lane, solo_acc(p, base));
+}
+
+// a4 + a5: the rows in place, then the optimum of row N into misc[5], misc[6].
+template <bool DROP>
+__device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
+  int32_t* const rowbuf = (int32_t*)(base + p.off_rowbuf);
+  int32_t* const buf = rowbuf + p.pad;
+  long long* mi = (long long*)(base + p.off_misc);
+  const int n = (int)mi[0];
+  const bool rw = mi[9] != 0;
+  const int d_first = (int)mi[7], dl = (int)mi[8];
+  if ((int)rw != (int)mi[12]) {  // the pad left of column 0 reads as "invalid" on this axis
+    for (int i = lane; i < p.pad; i += 32) rowbuf[i] = rw ? INFV : NEG;
+    if (lane == 0) mi[12] = rw;
+  }
+  if (rw) {  // P(0, 0) = 0, P(0, r > 0) = infinity over every column the instance reaches
+    for (int t = lane; t <= dl; t += 32) buf[t] = t == 0 ? 0 : INFV;
+  } else {
+    for (int t = lane; t <= d_first; t += 32) buf[t] = 15;  // G_0(t) = 0
+  }
+  __syncwarp();
+  const int4* inf = (const int4*)(base + p.off_info);
+  const int32_t* aux = (const int32_t*)(base + p.off_aux);
+  const int2* ops = (const int2*)(base + p.off_rowp);
+  uint32_t* decrow = dec;
+  const int kp = p.kp;
+  const int dec_row_words = p.nq * 32;
+  int M = 15;
+#pragma unroll 1
+  for (int pos = 0; pos < n; ++pos) {
+    const int4 f = inf[pos];
+    const int d = f.x, K = f.y & 255;
+    if (rw) {
+      // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
+      dp_row_dispatch<1, true, DROP, true>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
+      __syncwarp();
+    } else {
+      dp_row_dispatch<1, true, DROP, false>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
+      __syncwarp();
+      // M_pos = G_pos(d) (tail collapse); G_pos(t) = M_pos on (d, d_next] for the next row
+      if (d >= 0)
+        M = buf[d];
+      else if (!DROP)
+        M = NEG | 15;
+      const int dn = f.w;
+      const int first = d + 1 > 0 ? d + 1 : 0;
+#pragma unroll 1
+      for (int t = first + lane; t <= dn; t += 32) buf[t] = M;
+      __syncwarp();
+    }
+    ops += kp;
+    decrow += dec_row_words;
+  }
+  // a5: the optimum of row N
+  if (rw) {  // r* = the largest finite column (reading R6)
+    int best = -1;
+    for (int t = lane; t <= dl; t += 32)
+      if (buf[t] < INFV) best = t;
+    best = __reduce_max_sync(0xffffffffu, best);
+    if (lane == 0) {
+      mi[5] = best;
+      mi[6] = best;
+    }
+  } else {  // Q* = G_N(T), t* = least t with G_N(t) = Q* (G_N non-decreasing on [0, d_N])
+    long long Qv, ts = 0;
+    if (dl < 0) {
+      Qv = M;
+    } else {
+      Qv = buf[dl];
+      int lo = 0, hi = dl;
+      while (lo < hi) {
+        const int step = (hi - lo + 32) / 32;
+        int x = lo + (lane + 1) * step - 1;
+        if (x > hi) x = hi;
+        const unsigned m = __ballot_sync(0xffffffffu, buf[x] >= Qv);
+        const int fl = __ffs(m) - 1;
+        const int nhi = fl == 0 ? min(lo + step - 1, hi) : min(lo + (fl + 1) * step - 1, hi);
+        const int nlo = fl == 0 ? lo : lo + fl * step;
+        lo = nlo;
+        hi = nhi;
+      }
+      ts = lo;
+    }
+    if (lane == 0) {
+      mi[5] = Qv >= 0 ? (Qv >> 4) : -1;
+      mi[6] = ts;
+    }
+  }
+  __syncwarp();
+}
+
+// a6-a8: backtrack, schedule times and outputs, stats.
+static __device__ __noinline__ void solo_finish(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
+  const Smem S = solo_smem(p, base, dec);
+  tail_backtrack<1, true>(p, S, 0, lane, 0);
+  tail_outputs<1>(p, S, 0, lane, solo_acc(p, base));
+}
+
+template <bool DROP>
+__global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* base = smem + (size_t)warp * p.solo_warp_bytes;
+  uint32_t* dec = p.dec_global + ((int64_t)blockIdx.x * IC_SOLO_WPC + warp) * p.dec_slab_words;
+  unsigned long long* acc = solo_acc(p, base);
+  if (lane < 8) acc[lane] = 0;
+  if (lane == 0) ((long long*)(base + p.off_misc))[12] = -1;  // pad contents: none yet
+  __syncwarp();
   for (;;) {
-    // ---- a1-a3: claim an instance and set it up (instances the DP never sees are written here)
     int64_t b;
-    do {
+    do {  // claim instances until one needs the DP (the others are answered in the setup)
       unsigned long long v = 0;
       if (lane == 0) v = atomicAdd(&p.work[0], 1ull);
       b = (int64_t)__shfl_sync(0xffffffffu, v, 0);
-    } while (b < p.B && tail_setup<1>(p, S, b, 0, lane, acc) != ST_OK);
+    } while (b < p.B && solo_setup(p, base, b, lane) != ST_OK);
     if (b >= p.B) break;
-    long long* mi = S.misc;
-    const int n = (int)mi[0];
-    const bool rw = mi[9] != 0;
-    const int d_first = (int)mi[7], dl = (int)mi[8];
-    if ((int)rw != padmode) {  // the pad left of column 0 reads as "invalid" on this axis
-      padmode = rw;
-      for (int i = lane; i < p.pad; i += 32) S.rowbuf[i] = rw ? INFV : NEG;
-    }
-    if (rw) {  // P(0, 0) = 0, P(0, r > 0) = infinity over every column the instance reaches
-      for (int t = lane; t <= dl; t += 32) buf[t] = t == 0 ? 0 : INFV;
-    } else {
-      for (int t = lane; t <= d_first; t += 32) buf[t] = 15;  // G_0(t) = 0
-    }
-    __syncwarp();
-    // ---- a4: the rows, in place
-    const int4* inf = S.info;
-    const int2* ops = S.rowp;
-    uint32_t* decrow = S.dec;
-    int M = 15;
-#pragma unroll 1
-    for (int pos = 0; pos < n; ++pos) {
-      const int4 f = inf[pos];
-      const int d = f.x, K = f.y & 255;
-      if (rw) {
-        // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
-        dp_row_dispatch<1, true, DROP, true>(K, false, buf, buf, decrow, (const int4*)ops, d, 0, p.pad,
-                                             S.aux[pos]);
-        __syncwarp();
-      } else {
-        const bool gen = (f.y >> 8) & 1;
-        dp_row_dispatch<1, true, DROP, false>(K, gen, buf, buf, decrow, (const int4*)ops, d, f.z, p.pad, 0);
-        __syncwarp();
-        // M_pos = G_pos(d) (tail collapse); G_pos(t) = M_pos on (d, d_next] for the next row
-        if (d >= 0)
-          M = buf[d];
-        else if (!DROP)
-          M = NEG | 15;
-        const int dn = f.w;
-        if (dn > d) {
-          const int first = d + 1 > 0 ? d + 1 : 0;
-          for (int t = first + lane; t <= dn; t += 32) buf[t] = M;
-        }
-        __syncwarp();
-      }
-      ops += kp;
-      decrow += dec_row_words;
-    }
-    // ---- a5: the optimum of row N
-    if (rw) {  // r* = the largest finite column (reading R6)
-      int best = -1;
-      for (int t = lane; t <= dl; t += 32)
-        if (buf[t] < INFV) best = t;
-      best = __reduce_max_sync(0xffffffffu, best);
-      if (lane == 0) {
-        mi[5] = best;
-        mi[6] = best;
-      }
-    } else {  // Q* = G_N(T), t* = least t with G_N(t) = Q* (G_N non-decreasing on [0, d_N])
-      long long Qv, ts = 0;
-      if (dl < 0) {
-        Qv = M;
-      } else {
-        Qv = buf[dl];
-        int lo = 0, hi = dl;
-        while (lo < hi) {
-          const int step = (hi - lo + 32) / 32;
-          int x = lo + (lane + 1) * step - 1;
-          if (x > hi) x = hi;
-          const unsigned m = __ballot_sync(0xffffffffu, buf[x] >= Qv);
-          const int fl = __ffs(m) - 1;
-          const int nhi = fl == 0 ? min(lo + step - 1, hi) : min(lo + (fl + 1) * step - 1, hi);
-          const int nlo = fl == 0 ? lo : lo + fl * step;
-          lo = nlo;
-          hi = nhi;
-        }
-        ts = lo;
-      }
-      if (lane == 0) {
-        mi[5] = Qv >= 0 ? (Qv >> 4) : -1;
-        mi[6] = ts;
-      }
-    }
-    __syncwarp();
-    // ---- a6-a8
-    tail_backtrack<1, true>(p, S, 0, lane, 0);
-    tail_outputs<1>(p, S, 0, lane, acc);
+    solo_sweep<DROP>(p, base, dec, lane);
+    solo_finish(p, base, dec, lane);
   }
-  if (lane == 0 && p.stats) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (acc[i]) atomicAdd(&p.stats[i], acc[i]);
-  }
+  __syncwarp();
+  if (lane < 8 && p.stats && acc[lane]) atomicAdd(&p.stats[lane], acc[lane]);
   if (lane == 0) {  // the last warp out resets the counters for the next launch
     __threadfence();
     if (atomicAdd(&p.work[1], 1ull) == (unsigned long long)gridDim.x * IC_SOLO_WPC - 1) {

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build libicsched.so from git revision $1 into ab/$2.so (A/B timing on one box:
-# IC_SCHED_LIB=ab/$2.so python bench.py ...).  Scratch tool; ab/ is git-ignored.
+# python bench.py --lib ab/$2.so ...).  Scratch tool; ab/ is git-ignored.
 set -e
 rev=$1; name=$2
 root=$(cd "$(dirname "$0")/.." && pwd)
