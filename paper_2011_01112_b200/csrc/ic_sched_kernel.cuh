@@ -129,7 +129,10 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
                                        const int4* __restrict__ ops4, const int4 (&pre)[4], const int d,
                                        const int r, const int kr, const int lim) {
   constexpr int NT = 32 * NW;
-  constexpr int KK = GEN ? KMAX : K;
+  // the solo kernel's general path loops over the options at run time, reading each from
+  // shared memory (no option registers: it keeps the row loop's registers from spilling)
+  constexpr bool RTK = GEN && SB && NW == 1;
+  constexpr int KK = RTK ? 0 : GEN ? KMAX : K;
   // one-warp rows are swept by warp 0 of the warp-specialised kernel or by any warp of the
   // solo kernel: the lane is the thread's column offset there
   const int tid = NW == 1 ? (int)(threadIdx.x & 31) : (int)threadIdx.x, warp = NW == 1 ? 0 : tid >> 5;
@@ -149,7 +152,28 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   const int w0 = warp * 32;
   const int ng = d >= w0 ? (d - w0) / NT + 1 : 0;  // this warp's groups holding a column t <= d
   auto cell = [&](int t) -> int {
-    if constexpr (RW) {
+    if constexpr (RTK) {
+      const int2* o2 = (const int2*)ops4;
+      if constexpr (RW) {
+        int a = INFV;
+#pragma unroll 1
+        for (int k = 0; k < kr; ++k) {
+          const int2 o = o2[k];
+          a = __viaddmin_s32(cur[max(t - o.x, -1)], o.y, a);
+        }
+        a = a <= lim ? a : INFV;
+        return DROP ? min(cur[t], a) : a;
+      } else {
+        int v = DROP ? cur[t] : NEG;
+#pragma unroll 1
+        for (int k = 0; k < kr; ++k) {
+          const int2 o = o2[k];
+          const int src = t - o.x;
+          v = viaddmax(cur[src >= r ? src : -1], o.y, v);
+        }
+        return v;
+      }
+    } else if constexpr (RW) {
       int a = INFV;
 #pragma unroll
       for (int k = 0; k < KK; ++k) {
@@ -288,16 +312,18 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 }
 
 // gen: the row takes the general path (releases, or an option longer than the pad).
-template <int NW, bool SB, bool DROP, bool RW>
+// KC: the largest option count with its own unrolled sweep; rows with more take the
+// general path (the solo kernel compiles K <= 9, i.e. up to 8 optional stages).
+template <int NW, bool SB, bool DROP, bool RW, int KC = 15>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
                                                 uint32_t* decrow, const int4* ops4, int d, int r, int lim) {
   const int4 pre[4] = {ops4[0], ops4[1], ops4[2], ops4[3]};  // issued ahead of the K dispatch
-  if (gen) {
+  if (gen || K > KC) {
     dp_row<NW, SB, DROP, KMAX, true, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: dp_row<NW, SB, DROP, KK, false, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim); break;
+  case KK: if constexpr (KK <= KC) dp_row<NW, SB, DROP, KK, false, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)

@@ -26,6 +26,9 @@
 #ifndef IC_SOLO_WPC
 #define IC_SOLO_WPC 4  // warps per CTA (independent instances; a CTA is only a packing unit)
 #endif
+#ifndef IC_SOLO_KC
+#define IC_SOLO_KC 9  // option counts with an unrolled sweep (more: the general path)
+#endif
 #ifndef IC_SOLO_MINB
 #define IC_SOLO_MINB 7  // CTAs per SM the register budget is sized for (28 warps)
 #endif
@@ -96,10 +99,10 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
     const int d = f.x, K = f.y & 255;
     if (rw) {
       // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
-      dp_row_dispatch<1, true, DROP, true>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
+      dp_row_dispatch<1, true, DROP, true, IC_SOLO_KC>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
       __syncwarp();
     } else {
-      dp_row_dispatch<1, true, DROP, false>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
+      dp_row_dispatch<1, true, DROP, false, IC_SOLO_KC>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
       __syncwarp();
       // M_pos = G_pos(d) (tail collapse); G_pos(t) = M_pos on (d, d_next] for the next row
       if (d >= 0)
