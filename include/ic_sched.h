@@ -199,11 +199,16 @@ int ic_sched_solve_batch_state(ic_sched* h, const ic_batch_in* in, ic_batch_out*
                                void* cuda_stream);
 int ic_sched_replan_batch(ic_sched* h, const ic_batch_in* in, void* state, ic_batch_out* out, void* cuda_stream);
 
-/* Launch geometry chosen at create time (for tests, bench and profiling). */
+/* Launch geometry chosen at create time (for tests, bench and profiling).  The fields describe
+ * the kernel plain solves run first (the one-warp-per-instance kernel for H <= 1024 rows or
+ * the hybrid below, else the warp-specialised kernel).  hybrid = 1: fixed Delta with short
+ * reward rows (N * floor(1e6 / Delta) + 1 <= 1024) but a longer horizon; a solve is then two
+ * launches, the second over the instances whose sweep did not fit the first's row. */
 typedef struct {
   int32_t threads_per_cta, cols_per_thread, ctas_per_sm, grid;
   int32_t smem_bytes, decisions_in_smem, double_buffered, pad_cols;
   int64_t workspace_bytes;
+  int32_t kernels_per_solve, hybrid;
 } ic_sched_info;
 int ic_sched_get_info(const ic_sched* h, ic_sched_info* info);
 

@@ -69,7 +69,8 @@ class SchedTuning(ctypes.Structure):
 class SchedInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("threads_per_cta", "cols_per_thread", "ctas_per_sm", "grid",
                                               "smem_bytes", "decisions_in_smem", "double_buffered",
-                                              "pad_cols")] + [("workspace_bytes", ctypes.c_int64)]
+                                              "pad_cols")] + [("workspace_bytes", ctypes.c_int64)] + \
+        [(n, ctypes.c_int32) for n in ("kernels_per_solve", "hybrid")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -82,9 +82,9 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
 
 // One warp's private region in the solo kernel (ic_solo_kernel.cuh): a single in-place row
 // and one slot of the per-task tables.  Offsets are relative to the warp's base.
-Layout make_solo_layout(const ic_sched_config& c, int pad) {
+Layout make_solo_layout(const ic_sched_config& c, int pad, int cap_cols = 0) {
   Layout L{};
-  const int cols = (c.max_horizon + 31) / 32;
+  const int cols = ((cap_cols ? cap_cols : c.max_horizon) + 31) / 32;
   const int cap = 32 * cols;
   const int mt = c.max_tasks;
   L.nq = (cols + 7) / 8;
@@ -141,6 +141,11 @@ struct ic_sched {
   // solo kernel (one warp per instance) for plain solves when chosen; the state / re-plan
   // entry points always use the warp-specialised kernel above
   KernelFn solo_fn;
+  int hybrid;                 // 1: the solo kernel's row holds the reward axis only (fixed Delta,
+                              // long horizon); instances it cannot sweep go to the ws kernel
+  int64_t* defer_ids;         // [defer_cap] ids the solo kernel deferred; defer_n = their count
+  unsigned long long* defer_n;
+  int64_t defer_cap;
   Layout SL;
   int solo_grid, solo_ctas_per_sm;
   uint32_t* solo_dec;
@@ -284,10 +289,18 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   // is asked for (tuning.kernel = 1); tuning.kernel = 2 forces it at any horizon
   const bool ws_knobs = tu.dp_warps || tu.in_place || tu.slots || tu.decisions || tu.option_tables;
   const bool solo = tu.kernel == 2 || (tu.kernel == 0 && !ws_knobs && nw == 1 && !sb);
-  if (solo) {
+  // Hybrid: with a fixed Delta every reward-axis row has at most N * floor(1e6 / Delta) + 1
+  // columns (C3 at the paper's Delta = 0.1: 641).  When that is one warp's row but the
+  // horizon is not, the solo kernel sweeps every instance whose chosen axis fits that row
+  // (the reward axis, or a time axis with all deadlines below it) and defers the rest to
+  // the warp-specialised kernel in a second launch.
+  const int64_t qcap = c.delta_micro ? (int64_t)c.max_tasks * (1000000 / c.delta_micro) + 1 : (int64_t)1 << 40;
+  const bool hybrid = !solo && tu.kernel == 0 && !ws_knobs && !tu.axis && qcap <= 1024 && c.max_horizon > 1024;
+  if (solo || hybrid) {
     int rc = IC_OK;
     const int spad = tu.pad_cols ? ((tu.pad_cols + 31) & ~31) : 64 > c.max_horizon ? ((c.max_horizon + 31) & ~31) : 64;
-    Layout S = make_solo_layout(c, spad);
+    Layout S = make_solo_layout(c, spad, hybrid ? (int)qcap : 0);
+    h->hybrid = hybrid ? 1 : 0;
     KernelFn sf = icsched::kernel_solo(drop);
     const int bytes = S.bytes * IC_SOLO_WPC;
     int sp = 0;
@@ -323,6 +336,8 @@ extern "C" int ic_sched_destroy(ic_sched* h) {
   if (h->dec_global) cudaFree(h->dec_global);
   if (h->rowp_g) cudaFree(h->rowp_g);
   if (h->solo_dec) cudaFree(h->solo_dec);
+  if (h->defer_ids) cudaFree(h->defer_ids);
+  if (h->defer_n) cudaFree(h->defer_n);
   if (h->work) cudaFree(h->work);
   if (h->stage) cudaFree(h->stage);
   if (h->s_in) {
@@ -348,8 +363,12 @@ extern "C" int ic_sched_get_info(const ic_sched* h, ic_sched_info* info) {
     info->double_buffered = 0;
     info->pad_cols = h->SL.pad;
     info->workspace_bytes = h->solo_dec_warp_words * 4 * h->solo_grid * IC_SOLO_WPC;
+    info->kernels_per_solve = h->hybrid ? 2 : 1;
+    info->hybrid = h->hybrid;
     return IC_OK;
   }
+  info->kernels_per_solve = 1;
+  info->hybrid = 0;
   info->threads_per_cta = 32 * (h->nw + 1);
   info->cols_per_thread = (h->cfg.max_horizon + 32 * h->nw - 1) / (32 * h->nw);
   info->ctas_per_sm = h->ctas_per_sm;
@@ -487,8 +506,22 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.rowp_slab = h->rowp_slab;
   p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
                ((uintptr_t)p.opt_gain & 15) == 0 && !h->no_vec_loads;
+  const Params pw = p;  // the warp-specialised kernel's parameters
   if (h->solo_fn && !state) {  // one warp per instance (ic_solo_kernel.cuh)
     const Layout& S = h->SL;
+    if (h->hybrid) {  // room for every id the solo kernel may defer, and a zeroed count
+      if (in->n_instances > h->defer_cap) {
+        if (h->defer_ids) cudaFree(h->defer_ids);
+        h->defer_ids = nullptr;
+        h->defer_cap = 0;
+        if (cudaMalloc(&h->defer_ids, (size_t)in->n_instances * 8) != cudaSuccess) return IC_ERR_OOM;
+        h->defer_cap = in->n_instances;
+      }
+      if (!h->defer_n && cudaMalloc(&h->defer_n, 8) != cudaSuccess) return IC_ERR_OOM;
+      if (cudaMemsetAsync(h->defer_n, 0, 8, (cudaStream_t)cuda_stream) != cudaSuccess) return IC_ERR_CUDA;
+      p.defer_ids = h->defer_ids;
+      p.defer_n = h->defer_n;
+    }
     p.pad = S.pad;
     p.nq = S.nq;
     p.np2 = S.np2;
@@ -520,6 +553,14 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
     const int64_t need = (in->n_instances + IC_SOLO_WPC - 1) / IC_SOLO_WPC;
     if (grid > need) grid = need;
     h->solo_fn<<<(unsigned)grid, 32 * IC_SOLO_WPC, S.bytes * IC_SOLO_WPC, (cudaStream_t)cuda_stream>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return IC_ERR_CUDA;
+    if (!h->hybrid) return IC_OK;
+    // the deferred instances: the warp-specialised kernel over the listed ids (its CTAs
+    // exit at once when the list is empty)
+    Params q = pw;
+    q.ids = h->defer_ids;
+    q.nids = h->defer_n;
+    h->fn<<<(unsigned)h->grid, 32 * (h->nw + 1), h->L.bytes, (cudaStream_t)cuda_stream>>>(q);
     return cudaGetLastError() == cudaSuccess ? IC_OK : IC_ERR_CUDA;
   }
   int64_t grid = h->grid;

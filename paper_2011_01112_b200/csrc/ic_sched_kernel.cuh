@@ -88,6 +88,13 @@ struct Params {
   int replan;  // 1: the last task of each instance is a new arrival; rows before it are kept
   int ckpt;    // rows kept in the state: every ckpt-th (rows ckpt-1, 2 ckpt-1, ...), power of two
   unsigned long long* work;  // [2] dynamic instance counter, CTAs finished (reset by the last CTA)
+  // hybrid solves (fixed Delta, long horizon): the solo kernel runs the instances whose sweep
+  // fits its short row and lists the others in defer_ids; the warp-specialised kernel then
+  // solves exactly the listed ids (ids / nids non-null)
+  int64_t* defer_ids;
+  unsigned long long* defer_n;
+  const int64_t* ids;
+  const unsigned long long* nids;
   int rowbuf_stride;  // ints per row buffer (pad + capacity)
   // large task sets: the tail warp's option tables of both slots live in a per-CTA global
   // (L2) slab and the DP warps copy the current one into their single shared-memory table
@@ -603,6 +610,13 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
   // budget-tracked backtrack, so they stay on the time axis.
   const bool rw = p.axis_mode != 1 && !anyrel && qcarry + 1 <= p.cap && (!p.state || qcarry < p.H) &&
                  (p.axis_mode == 2 || wr < wt);
+  if (!rw && p.defer_ids && S.info[s * p.max_tasks + n - 1].x >= p.cap) {
+    // the time axis does not fit this kernel's row (the solo kernel sized for the reward
+    // axis): hand the instance to the warp-specialised kernel's second launch
+    if (lane == 0) p.defer_ids[atomicAdd(p.defer_n, 1ull)] = b;
+    __syncwarp();
+    return ST_BAD + 200;
+  }
   if (rw) {
     for (int pos = lane; pos < n; pos += 32) {
       int4* f = S.info + s * p.max_tasks + pos;
@@ -722,6 +736,28 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
     }
   }
   __syncwarp();
+}
+
+// After the backtrack the instance's decision nibbles are dead: invalidate their L2 lines
+// (discard.global.L2, no write-back) so they never travel to HBM.  Row pos wrote
+// ceil(groups / 8) chunks of NT words from the start of its row (the active columns
+// t <= info.x: the deadline, or Qpre on the reward axis).  Only for the per-CTA scratch
+// buffers; decisions kept in a caller's re-plan state are not touched.
+template <int NW>
+__device__ __forceinline__ void discard_decisions(const Params& p, const Smem& S, int s, int lane, int db) {
+  constexpr int NT = 32 * NW;
+  if (p.state || p.dec_smem) return;
+  const int n = (int)S.misc[s * 16];
+  const int4* inf = S.info + s * p.max_tasks;
+  const char* base = (const char*)(S.dec + db * p.dec_words);
+  const int64_t row_bytes = (int64_t)p.nq * NT * 4;
+  for (int pos = 0; pos < n; ++pos) {
+    const int cols = inf[pos].x + 1;
+    if (cols <= 0) continue;
+    const int lines = (((cols - 1) / NT) / 8 + 1) * NW;  // 128-byte lines: NT * 4 / 128 per chunk
+    for (int l = lane; l < lines; l += 32)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + pos * row_bytes + (int64_t)l * 128) : "memory");
+  }
 }
 
 // a7/a8: EDF schedule (warp max-plus scan), outputs in input order, stats.
@@ -853,7 +889,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     auto claim = [&]() -> int64_t {
       unsigned long long v = 0;
       if (lane == 0) v = atomicAdd(&p.work[0], 1ull);
-      return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+      v = __shfl_sync(0xffffffffu, v, 0);
+      if (p.ids) return v < *p.nids ? p.ids[v] : p.B;  // the instances the solo kernel deferred
+      return (int64_t)v;
     };
     int64_t b = claim();
     while (b < p.B && tail_setup<NW>(p, S, b, 0, lane, acc) != ST_OK) b = claim();
@@ -875,8 +913,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         if (p.ndec == 2) {
           bar_arrive(BAR_READY, NT + 32);  // nb sweeps into the other decision buffer
           tail_backtrack<NW>(p, S, s, lane, db);
+          discard_decisions<NW>(p, S, s, lane, db);
         } else {
           tail_backtrack<NW>(p, S, s, lane, db);
+          discard_decisions<NW>(p, S, s, lane, db);
+          __syncwarp();
           bar_arrive(BAR_READY, NT + 32);  // decisions free: the DP warps may start nb
         }
         tail_outputs<NW>(p, S, s, lane, acc);
@@ -887,6 +928,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       while (b < p.B) {
         bar_sync(BAR_DONE, NT + 32);
         tail_backtrack<NW>(p, S, 0, lane, 0);
+        discard_decisions<NW>(p, S, 0, lane, 0);
         tail_outputs<NW>(p, S, 0, lane, acc);
         int64_t nb = claim();
         while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb = claim();

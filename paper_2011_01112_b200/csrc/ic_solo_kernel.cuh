@@ -160,6 +160,7 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
 static __device__ __noinline__ void solo_finish(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
   const Smem S = solo_smem(p, base, dec);
   tail_backtrack<1, true>(p, S, 0, lane, 0);
+  discard_decisions<1>(p, S, 0, lane, 0);
   tail_outputs<1>(p, S, 0, lane, solo_acc(p, base));
 }
 

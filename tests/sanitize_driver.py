@@ -26,6 +26,9 @@ VARIANTS = {
     "sb8_inplace": (dict(in_place=1, dp_warps=8), "C3", 2, 0),
     "nw16_global_tables": (dict(in_place=1, dp_warps=16, option_tables=1), "C3", 2, 0),
     "reward_axis": (dict(axis=2, kernel=1), "C2", 6, 100_000),
+    "solo": ({}, "C2", 6, 0),
+    "solo_reward": ({}, "C2", 6, 100_000),
+    "hybrid": ({}, "C3", 3, 100_000),
 }
 EXTRA = ("replan", "reassign")
 

@@ -398,3 +398,22 @@ def test_solo_and_warp_specialised_kernels_agree(name, n, delta, mode):
                         delta=delta, eps=cw.epsilon_micro, tuning=dict(kernel=kernel))
         assert_parity(got, ref, f"{name} kernel={kernel} delta={delta} mode={mode}")
         assert (got["_info"]["threads_per_cta"] == 128) == (kernel != 1)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_hybrid_reward_rows(mode):
+    """Fixed Delta = 0.1 at H = 4096 (C3 shape): the solo kernel sweeps the instances whose
+    reward-axis rows fit it and defers the rest (releases force the time axis; a time axis
+    past its row) to the warp-specialised kernel.  Every instance equals the oracle."""
+    cw = gen.CONFIGS["C3"]
+    rng = np.random.default_rng(120 + mode)
+    rel = gen.tiny_random(rng, 400, max_tasks=12, max_opt=8, horizon=4096, p_release=0.6)
+    rel.mand_wcet[:] = rel.mand_wcet * 50
+    short = gen.tiny_random(rng, 400, max_tasks=12, max_opt=8, horizon=600, p_release=0.0)
+    batch = gen.concat([gen.generate(cw, 300), rel, short], cw.n_opt)
+    ocfg = OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=64, max_horizon=4096)
+    ref = oracle.solve(batch, ocfg, TIME)
+    got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode, delta=100_000)
+    assert got["_info"]["hybrid"] == 1 and got["_info"]["kernels_per_solve"] == 2
+    assert_parity(got, ref, f"hybrid mode={mode}")
+    np.testing.assert_array_equal(got["stats"], stats_from(got, batch))
