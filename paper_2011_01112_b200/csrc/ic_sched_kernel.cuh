@@ -751,12 +751,11 @@ __device__ __forceinline__ void discard_decisions(const Params& p, const Smem& S
   const int4* inf = S.info + s * p.max_tasks;
   const char* base = (const char*)(S.dec + db * p.dec_words);
   const int64_t row_bytes = (int64_t)p.nq * NT * 4;
-  for (int pos = 0; pos < n; ++pos) {
+  for (int pos = lane; pos < n; pos += 32) {  // a lane per row
     const int cols = inf[pos].x + 1;
-    if (cols <= 0) continue;
-    const int lines = (((cols - 1) / NT) / 8 + 1) * NW;  // 128-byte lines: NT * 4 / 128 per chunk
-    for (int l = lane; l < lines; l += 32)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + pos * row_bytes + (int64_t)l * 128) : "memory");
+    const int lines = cols > 0 ? (((cols - 1) / NT) / 8 + 1) * NW : 0;  // 128-byte lines: NW per chunk
+    const char* row = base + pos * row_bytes;
+    for (int l = 0; l < lines; ++l) asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + l * 128) : "memory");
   }
 }
 

@@ -76,7 +76,9 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
   const int n = (int)mi[0];
   const bool rw = mi[9] != 0;
   const int d_first = (int)mi[7], dl = (int)mi[8];
-  if ((int)rw != (int)mi[12]) {  // the pad left of column 0 reads as "invalid" on this axis
+  const bool refill = (int)rw != (int)mi[12];
+  __syncwarp();
+  if (refill) {  // the pad left of column 0 reads as "invalid" on this axis
     for (int i = lane; i < p.pad; i += 32) rowbuf[i] = rw ? INFV : NEG;
     if (lane == 0) mi[12] = rw;
   }
