@@ -746,6 +746,9 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
 template <int NW>
 __device__ __forceinline__ void discard_decisions(const Params& p, const Smem& S, int s, int lane, int db) {
   constexpr int NT = 32 * NW;
+#ifdef IC_NO_DISCARD
+  return;
+#endif
   if (p.state || p.dec_smem) return;
   const int n = (int)S.misc[s * 16];
   const int4* inf = S.info + s * p.max_tasks;
