@@ -24,13 +24,13 @@
 #include "ic_sched_kernel.cuh"
 
 #ifndef IC_SOLO_WPC
-#define IC_SOLO_WPC 4  // warps per CTA (independent instances; a CTA is only a packing unit)
+#define IC_SOLO_WPC 1  // warps per CTA (independent instances; 1: the finest shared-memory packing)
 #endif
 #ifndef IC_SOLO_KC
 #define IC_SOLO_KC 9  // option counts with an unrolled sweep (more: the general path)
 #endif
 #ifndef IC_SOLO_MINB
-#define IC_SOLO_MINB 7  // CTAs per SM the register budget is sized for (28 warps)
+#define IC_SOLO_MINB 28  // CTAs per SM the register budget is sized for (28 warps, 72 registers)
 #endif
 
 namespace icsched {

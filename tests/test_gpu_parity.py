@@ -397,7 +397,7 @@ def test_solo_and_warp_specialised_kernels_agree(name, n, delta, mode):
         got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
                         delta=delta, eps=cw.epsilon_micro, tuning=dict(kernel=kernel))
         assert_parity(got, ref, f"{name} kernel={kernel} delta={delta} mode={mode}")
-        assert (got["_info"]["threads_per_cta"] == 128) == (kernel != 1)
+        assert (got["_info"]["threads_per_cta"] == 32) == (kernel != 1)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
