@@ -48,6 +48,11 @@ typedef struct {
   uint32_t prior_micro;  /* planner's confidence prior before a request's first stage */
   int32_t device;
   int32_t period;        /* 0: closed loop (think); > 0: open loop, mean gap in ticks */
+  int32_t plan_cells_per_tick; /* scheduler cost model: > 0: every plan
+                                  holds the server for ceil(cells / plan_cells_per_tick) ticks
+                                  before the next stage may start, cells = the size of the
+                                  paper's reward-indexed table, sum_i (Qpre_i + 1)(S_i + 1);
+                                  0: planning is free (the GPU-batched solver's view) */
 } ic_sim_config;
 
 typedef struct {
@@ -56,9 +61,31 @@ typedef struct {
   double accuracy;        /* conf_micro / 1e6 / requests (misses count 0) */
   double miss_rate, mean_depth;
   double sim_seconds, gpu_seconds;
+  int64_t plan_ticks, busy_ticks; /* ticks spent planning (cost model) and running stages */
 } ic_sim_result;
 
+/* Parity hook: a copy of the first planner batches the simulator sent to the solver, inputs
+ * (the ic_batch_in layout, opt_* rows with stride n_opt) and the solver's outputs, until
+ * either capacity is reached (whole batches only).  All pointers are caller-owned host
+ * buffers of the stated capacities; n_instances / n_tasks report what was written. */
+typedef struct {
+  int64_t cap_instances, cap_tasks;
+  int64_t n_instances, n_tasks;
+  int64_t* task_begin;  /* [cap_instances + 1] */
+  int32_t *release, *deadline, *mand_wcet;
+  uint8_t* n_opt;
+  int32_t* opt_wcet;    /* [cap_tasks][n_opt] */
+  uint32_t* mand_conf;
+  int32_t* opt_gain;    /* [cap_tasks][n_opt] */
+  int8_t* kept;
+  int32_t *start, *finish;
+  int64_t *q_total, *conf_micro;
+  int32_t* makespan;
+  uint8_t* status;
+} ic_sim_dump;
+
 int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out);
+int ic_sim_run_dump(const ic_sim_config* cfg, ic_sim_result* out, ic_sim_dump* dump);
 
 #ifdef __cplusplus
 }

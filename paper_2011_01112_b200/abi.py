@@ -92,7 +92,8 @@ class _GenCfg(ctypes.Structure):
 
 EXPORTED = ("ic_sched_create", "ic_sched_create_tuned", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
             "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch", "ic_sched_state_bytes",
-            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sim_run", "ic_probe_smem")
+            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sim_run", "ic_sim_run_dump",
+            "ic_probe_smem")
 
 IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
 
@@ -113,35 +114,65 @@ class SimConfig(ctypes.Structure):
                 ("wcet_base", ctypes.c_int32), ("d_lo", ctypes.c_int32), ("d_hi", ctypes.c_int32),
                 ("think", ctypes.c_int32), ("seed", ctypes.c_uint64), ("policy", ctypes.c_int32),
                 ("utility", ctypes.c_int32), ("delta_micro", ctypes.c_uint32), ("prior_micro", ctypes.c_uint32),
-                ("device", ctypes.c_int32), ("period", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("period", ctypes.c_int32), ("plan_cells_per_tick", ctypes.c_int32)]
 
     def __init__(self, servers=1, clients=20, requests_per_client=50, n_opt=7, wcet_base=10, d_lo=10,
                  d_hi=300, think=1, seed=0x2011011106, policy=IC_SIM_PLANNER, utility=IC_SIM_UTIL_EXP,
-                 delta_micro=100_000, prior_micro=500_000, device=0, period=0):
+                 delta_micro=100_000, prior_micro=500_000, device=0, period=0, plan_cells_per_tick=0):
         if isinstance(policy, str):
             policy = SIM_POLICIES[policy]
         super().__init__(servers, clients, requests_per_client, n_opt, wcet_base, d_lo, d_hi, think, seed,
-                         policy, utility, delta_micro, prior_micro, device, period)
+                         policy, utility, delta_micro, prior_micro, device, period, plan_cells_per_tick)
 
 
 class SimResult(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("requests", "misses", "stages_run", "plans", "rounds",
                                               "conf_micro")] + \
                [(n, ctypes.c_double) for n in ("accuracy", "miss_rate", "mean_depth", "sim_seconds",
-                                               "gpu_seconds")]
+                                               "gpu_seconds")] + \
+               [(n, ctypes.c_int64) for n in ("plan_ticks", "busy_ticks")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
-def simulate(cfg: SimConfig) -> dict:
-    """ic_sim_run: event-driven edge-server simulation (include/ic_sim.h, NEXT-4)."""
+_DUMP_FIELDS = (("task_begin", np.int64, "csr"), ("release", np.int32, "task"), ("deadline", np.int32, "task"),
+                ("mand_wcet", np.int32, "task"), ("n_opt", np.uint8, "task"), ("opt_wcet", np.int32, "task_opt"),
+                ("mand_conf", np.uint32, "task"), ("opt_gain", np.int32, "task_opt"), ("kept", np.int8, "task"),
+                ("start", np.int32, "task"), ("finish", np.int32, "task"), ("q_total", np.int64, "instance"),
+                ("conf_micro", np.int64, "instance"), ("makespan", np.int32, "instance"),
+                ("status", np.uint8, "instance"))
+
+
+class _SimDump(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("cap_instances", "cap_tasks", "n_instances", "n_tasks")] + \
+               [(n, ctypes.c_void_p) for n, _, _ in _DUMP_FIELDS]
+
+
+def simulate(cfg: SimConfig, dump_instances: int = 0, dump_tasks: int = 0):
+    """ic_sim_run: event-driven edge-server simulation (include/ic_sim.h, NEXT-4).
+
+    With dump_instances > 0 (ic_sim_run_dump) also returns the first planner batches the
+    simulator sent to the solver: inputs in the ic_batch_in layout and the solver's outputs."""
     lib = load_library()
     r = SimResult()
-    rc = lib.ic_sim_run(ctypes.byref(cfg), ctypes.byref(r))
+    if not dump_instances:
+        rc = lib.ic_sim_run(ctypes.byref(cfg), ctypes.byref(r))
+        if rc != 0:
+            raise ICSchedError("ic_sim_run", rc)
+        return r.as_dict()
+    cap_t = dump_tasks or dump_instances * cfg.clients * 4
+    bufs = {n: np.zeros(((cap_t, cfg.n_opt) if k == "task_opt" else
+                         (dump_instances + 1 if k == "csr" else cap_t if k == "task" else dump_instances)), dt)
+            for n, dt, k in _DUMP_FIELDS}
+    d = _SimDump(dump_instances, cap_t, 0, 0, *[_ptr(bufs[n]) if bufs[n].size else None for n, _, _ in _DUMP_FIELDS])
+    rc = lib.ic_sim_run_dump(ctypes.byref(cfg), ctypes.byref(r), ctypes.byref(d))
     if rc != 0:
-        raise ICSchedError("ic_sim_run", rc)
-    return r.as_dict()
+        raise ICSchedError("ic_sim_run_dump", rc)
+    B, T = d.n_instances, d.n_tasks
+    out = {n: (v[:B + 1] if n == "task_begin" else v[:B] if k == "instance" else v[:T]) for (n, _, k), v in
+           zip(_DUMP_FIELDS, [bufs[n] for n, _, _ in _DUMP_FIELDS])}
+    return r.as_dict(), out
 
 
 PROBE_MODES = {"lds32": 0, "lds128": 1, "lds32_viaddmax": 2}
@@ -198,6 +229,7 @@ def load_library():
         lib.ic_sched_replan_batch.argtypes = [ctypes.c_void_p, P(_In), ctypes.c_void_p, P(_Out), ctypes.c_void_p]
         lib.ic_sched_state_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         lib.ic_sim_run.argtypes = [P(SimConfig), P(SimResult)]
+        lib.ic_sim_run_dump.argtypes = [P(SimConfig), P(SimResult), P(_SimDump)]
         lib.ic_probe_smem.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P(ctypes.c_double),
                                       P(ctypes.c_double), P(ctypes.c_double)]
         for f in EXPORTED:

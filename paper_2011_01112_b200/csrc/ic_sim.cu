@@ -28,6 +28,7 @@ struct Req {
 
 struct Server {
   int64_t now = 0, busy_until = NEVER;
+  int64_t plan_until = 0;  // cost model: no stage starts before the plan is ready
   int running = -1;  // index into reqs of the stage in flight
   bool dirty = false;
   int rr_last = -1;
@@ -42,6 +43,7 @@ struct Sim {
   int L;
   std::vector<Server> sv;
   int64_t requests = 0, misses = 0, stages = 0, plans = 0, rounds = 0, conf = 0;
+  int64_t plan_ticks = 0, busy_ticks = 0;
 };
 
 // A request's trace: deadline, stage WCETs, true confidence curve (the generator's recipe).
@@ -113,7 +115,7 @@ bool advance(Sim& S, Server& v) {
       const Req& q = v.reqs[i];
       if (q.s >= S.L || q.dabs <= v.now || (q.s > 0 && q.s >= q.planned)) answer(S, v, i, v.now);
     }
-    if (v.running < 0) {
+    if (v.running < 0 && v.now >= v.plan_until) {
       if (!v.reqs.empty()) {
         if (pol == IC_SIM_PLANNER && v.dirty) return true;
         int pick = -1;
@@ -145,6 +147,7 @@ bool advance(Sim& S, Server& v) {
         if (pick >= 0) {
           v.running = pick;
           v.busy_until = v.now + v.reqs[pick].w[v.reqs[pick].s];
+          S.busy_ticks += v.reqs[pick].w[v.reqs[pick].s];
           S.stages++;
         }
       }
@@ -156,7 +159,7 @@ bool advance(Sim& S, Server& v) {
       if (v.client_left[c] > 0) t_arr = std::min(t_arr, v.client_next[c]);
     for (int i = 0; i < (int)v.reqs.size(); ++i)
       if (i != v.running) t_arr = std::min(t_arr, v.reqs[i].dabs);
-    const int64_t t_done = v.running >= 0 ? v.busy_until : NEVER;
+    const int64_t t_done = v.running >= 0 ? v.busy_until : v.plan_until > v.now ? v.plan_until : NEVER;
     const int64_t t = std::min(t_arr, t_done);
     if (t >= NEVER) {
       v.done = true;
@@ -183,10 +186,13 @@ bool advance(Sim& S, Server& v) {
 }
 
 // The planner's DP instance of a server at a scheduling point (time origin = now, GPU free).
-void build_instance(const Sim& S, const Server& v, std::vector<int64_t>& tb, std::vector<int32_t>& rel,
-                    std::vector<int32_t>& dl, std::vector<int32_t>& mw, std::vector<uint8_t>& no,
-                    std::vector<int32_t>& ow, std::vector<uint32_t>& mc, std::vector<int32_t>& og) {
+// Returns the size of the paper's reward-indexed table for the instance (the scheduler cost
+// model): rows in EDF order, row i spanning Qpre_i + 1 reward columns with S_i + 2 options.
+int64_t build_instance(const Sim& S, const Server& v, std::vector<int64_t>& tb, std::vector<int32_t>& rel,
+                       std::vector<int32_t>& dl, std::vector<int32_t>& mw, std::vector<uint8_t>& no,
+                       std::vector<int32_t>& ow, std::vector<uint32_t>& mc, std::vector<int32_t>& og) {
   const int st = S.L - 1;
+  std::vector<std::pair<int64_t, int64_t>> rows;  // (deadline, max quantised reward) per task
   for (const Req& q : v.reqs) {
     // predicted cumulative confidence after each stage (completed stages are sunk)
     int64_t pred[KMAX];
@@ -214,17 +220,39 @@ void build_instance(const Sim& S, const Server& v, std::vector<int64_t>& tb, std
       ow.push_back(j < S.L ? q.w[j] : 0);
       og.push_back(j < S.L ? (int32_t)(pred[j] - pred[j - 1]) : 0);
     }
+    int64_t qm = 0;
+    for (int j = q.s; j < S.L; ++j) qm = std::max<int64_t>(qm, (pred[j] - base + carry) / S.c.delta_micro);
+    rows.push_back({q.dabs, qm * 16 + (S.L - q.s)});
   }
   tb.push_back(tb.back() + (int64_t)v.reqs.size());
+  std::sort(rows.begin(), rows.end());
+  int64_t qpre = 0, cells = 0;
+  for (const auto& r : rows) {
+    qpre += r.second >> 4;
+    cells += (qpre + 1) * ((r.second & 15) + 1);
+  }
+  return cells;
 }
 
 }  // namespace
 
-extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) {
+extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) { return ic_sim_run_dump(cfg, out, nullptr); }
+
+extern "C" int ic_sim_run_dump(const ic_sim_config* cfg, ic_sim_result* out, ic_sim_dump* dump) {
   if (!cfg || !out) return -1;
+  if (dump) {
+    if (dump->cap_instances < 0 || dump->cap_tasks < 0 || !dump->task_begin || !dump->release || !dump->deadline ||
+        !dump->mand_wcet || !dump->n_opt || !dump->mand_conf || !dump->kept || !dump->start || !dump->finish ||
+        !dump->q_total || !dump->conf_micro || !dump->makespan || !dump->status ||
+        (cfg->n_opt > 0 && (!dump->opt_wcet || !dump->opt_gain)))
+      return -1;
+    dump->n_instances = dump->n_tasks = 0;
+    dump->task_begin[0] = 0;
+  }
   const ic_sim_config c = *cfg;
   if (c.servers < 1 || c.clients < 1 || c.requests_per_client < 1 || c.n_opt < 0 || c.n_opt > KMAX - 1 ||
       c.wcet_base < 1 || c.d_lo < 1 || c.d_hi < c.d_lo || c.think < 1 || c.period < 0 || c.policy < 0 || c.policy > 3 ||
+      c.plan_cells_per_tick < 0 ||
       (c.policy == IC_SIM_PLANNER && c.delta_micro == 0))
     return -1;
   const auto t0 = std::chrono::steady_clock::now();
@@ -278,7 +306,8 @@ extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) {
     S.rounds++;
     tb.assign(1, 0);
     rel.clear(); dl.clear(); mw.clear(); no.clear(); ow.clear(); mc.clear(); og.clear();
-    for (int i : need) build_instance(S, S.sv[i], tb, rel, dl, mw, no, ow, mc, og);
+    std::vector<int64_t> cells;
+    for (int i : need) cells.push_back(build_instance(S, S.sv[i], tb, rel, dl, mw, no, ow, mc, og));
     const int64_t B = (int64_t)need.size(), T = tb.back();
     kept.resize(T); st.resize(T); fi.resize(T);
     qt.resize(B); cm.resize(B); ct.resize(B); ms.resize(B); status.resize(B);
@@ -294,8 +323,39 @@ extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) {
       return -3;
     }
     S.plans += B;
+    if (dump && dump->n_instances + B <= dump->cap_instances && dump->n_tasks + T <= dump->cap_tasks) {
+      const int64_t i0 = dump->n_instances, t0 = dump->n_tasks, so = c.n_opt;
+      for (int64_t b = 0; b < B; ++b) {
+        dump->task_begin[i0 + b + 1] = t0 + tb[b + 1];
+        dump->q_total[i0 + b] = qt[b];
+        dump->conf_micro[i0 + b] = cm[b];
+        dump->makespan[i0 + b] = ms[b];
+        dump->status[i0 + b] = status[b];
+      }
+      for (int64_t k = 0; k < T; ++k) {
+        dump->release[t0 + k] = rel[k];
+        dump->deadline[t0 + k] = dl[k];
+        dump->mand_wcet[t0 + k] = mw[k];
+        dump->n_opt[t0 + k] = no[k];
+        dump->mand_conf[t0 + k] = mc[k];
+        for (int64_t j = 0; j < so; ++j) {
+          dump->opt_wcet[(t0 + k) * so + j] = ow[k * so + j];
+          dump->opt_gain[(t0 + k) * so + j] = og[k * so + j];
+        }
+        dump->kept[t0 + k] = kept[k];
+        dump->start[t0 + k] = st[k];
+        dump->finish[t0 + k] = fi[k];
+      }
+      dump->n_instances += B;
+      dump->n_tasks += T;
+    }
     for (int64_t b = 0; b < B; ++b) {
       Server& v = S.sv[need[b]];
+      if (c.plan_cells_per_tick > 0) {  // the plan holds the server before the next stage
+        const int64_t cost = (cells[b] + c.plan_cells_per_tick - 1) / c.plan_cells_per_tick;
+        v.plan_until = v.now + cost;
+        S.plan_ticks += cost;
+      }
       for (int64_t k = tb[b]; k < tb[b + 1]; ++k) {
         Req& q = v.reqs[k - tb[b]];
         q.planned = kept[k] < 0 ? q.s : q.s + 1 + kept[k];  // DROP: stop here (answer now)
@@ -315,6 +375,8 @@ extern "C" int ic_sim_run(const ic_sim_config* cfg, ic_sim_result* out) {
   r.miss_rate = S.requests ? (double)S.misses / (double)S.requests : 0.0;
   r.mean_depth = S.requests ? (double)S.stages / (double)S.requests : 0.0;
   r.gpu_seconds = gpu_s;
+  r.plan_ticks = S.plan_ticks;
+  r.busy_ticks = S.busy_ticks;
   r.sim_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = r;
   return 0;

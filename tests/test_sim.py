@@ -103,3 +103,43 @@ def test_planner_oracle_utility_at_least_exp():
     exp = _run(utility=pkg.IC_SIM_UTIL_EXP, **kw)
     opt = _run(utility=pkg.IC_SIM_UTIL_ORACLE, **kw)
     assert opt["accuracy"] >= exp["accuracy"] - 0.01
+
+
+def test_invalid_cost_model_rejected():
+    with pytest.raises(pkg.ICSchedError) as e:
+        _run(policy="planner", plan_cells_per_tick=-1)
+    assert e.value.rc == -1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("utility,delta", [(0, 100_000), (1, 20_000), (0, 500_000)])
+def test_simulator_plans_equal_oracle(utility, delta):
+    """Parity hook: the DP instances the simulator's planner batched (sunk stages, carried
+    remainders, Exp predictions) and the plans the GPU returned for them equal the CPU
+    oracle's, element by element — the simulator's decisions are the paper's DP."""
+    import numpy as np
+    import oracle
+    from gen import Batch
+    from tests.gpu_util import assert_parity
+    cfg = pkg.SimConfig(servers=24, clients=14, requests_per_client=12, period=500, policy="planner",
+                        utility=utility, delta_micro=delta)
+    res, d = pkg.simulate(cfg, dump_instances=3000, dump_tasks=60000)
+    assert d["task_begin"].size - 1 >= 200
+    batch = Batch(d["task_begin"], d["release"], d["deadline"], d["mand_wcet"], d["n_opt"], d["opt_wcet"],
+                  d["mand_conf"], d["opt_gain"])
+    ocfg = oracle.OracleConfig(delta_micro=delta, max_tasks=4096, max_horizon=cfg.d_hi + 1)
+    ref = oracle.solve(batch, ocfg, oracle.TIME)
+    got = dict(d, conf_total=d["conf_micro"] / 1e6)
+    assert_parity(got, ref, f"simulator batches utility={utility} delta={delta}")
+    assert (oracle.check(batch, got, ocfg) == 0).all()
+
+
+@pytest.mark.gpu
+def test_plan_cost_model():
+    """with the scheduler's cost charged to the server, a finer reward step makes
+    the paper's table larger and the planning time longer; free planning charges nothing."""
+    kw = dict(servers=16, clients=16, requests_per_client=15, period=600, policy="planner")
+    free = _run(**kw)
+    assert free["plan_ticks"] == 0
+    ticks = [_run(delta_micro=d, plan_cells_per_tick=200, **kw)["plan_ticks"] for d in (500_000, 100_000, 20_000)]
+    assert 0 < ticks[0] < ticks[1] < ticks[2]
