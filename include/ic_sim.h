@@ -49,8 +49,9 @@ typedef struct {
   int32_t device;
   int32_t period;        /* 0: closed loop (think); > 0: open loop, mean gap in ticks */
   int32_t plan_cells_per_tick; /* scheduler cost model: > 0: every plan
-                                  holds the server for ceil(cells / plan_cells_per_tick) ticks
-                                  before the next stage may start, cells = the size of the
+                                  holds the server for cells / plan_cells_per_tick ticks (the
+                                  fraction carried to the server's next plan) before the next
+                                  stage may start, cells = the size of the
                                   paper's reward-indexed table, sum_i (Qpre_i + 1)(S_i + 1);
                                   0: planning is free (the GPU-batched solver's view) */
 } ic_sim_config;

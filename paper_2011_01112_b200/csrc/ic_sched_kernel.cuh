@@ -355,6 +355,60 @@ __device__ __forceinline__ unsigned long long warp_bitonic_sort(unsigned long lo
   return x;
 }
 
+// Ascending sort of key[0..n) by one warp (the EDF order, keys (d, r, index)): in registers
+// for n <= 64 (one or two keys per lane, bitonic network over shuffles), else a bitonic
+// network over shared memory (key must hold the next power of two >= n entries).
+__device__ __forceinline__ void warp_sort_keys(unsigned long long* key, int n, int lane) {
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  if (np2 <= 32) {
+    unsigned long long x = lane < n ? key[lane] : ~0ull;
+    x = warp_bitonic_sort(x, lane);
+    if (lane < n) key[lane] = x;
+  } else if (np2 == 64) {  // two keys per lane (positions lane, lane + 32), in registers
+    unsigned long long x0 = key[lane], x1 = lane + 32 < n ? key[lane + 32] : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j == 32) {  // k = 64: partners lane and lane + 32, ascending
+          const unsigned long long lo2 = x0 < x1 ? x0 : x1;
+          x1 = x0 < x1 ? x1 : x0;
+          x0 = lo2;
+        } else {
+          const unsigned long long y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+          const unsigned long long y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+          const bool lower = (lane & j) == 0;
+          const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+          x0 = (lower == up0) ? (x0 < y0 ? x0 : y0) : (x0 < y0 ? y0 : x0);
+          x1 = (lower == up1) ? (x1 < y1 ? x1 : y1) : (x1 < y1 ? y1 : x1);
+        }
+      }
+    }
+    key[lane] = x0;
+    if (lane + 32 < n) key[lane + 32] = x1;
+  } else {
+    for (int i = n + lane; i < np2; i += 32) key[i] = ~0ull;
+    __syncwarp();
+    for (int k = 2; k <= np2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < np2; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long a = key[i], c = key[ixj];
+            if ((a > c) == ((i & k) == 0)) {
+              key[i] = c;
+              key[ixj] = a;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ long long warp_sum64(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -496,53 +550,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     if (delta < 1) delta = 1;
   }
   // a3: EDF order
-  int np2 = 1;
-  while (np2 < n) np2 <<= 1;
-  if (np2 <= 32) {
-    unsigned long long x = lane < n ? S.key[lane] : ~0ull;
-    x = warp_bitonic_sort(x, lane);
-    if (lane < n) S.key[lane] = x;
-  } else if (np2 == 64) {  // two keys per lane (positions lane, lane + 32), in registers
-    unsigned long long x0 = S.key[lane], x1 = lane + 32 < n ? S.key[lane + 32] : ~0ull;
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        if (j == 32) {  // k = 64: partners lane and lane + 32, ascending
-          const unsigned long long lo2 = x0 < x1 ? x0 : x1;
-          x1 = x0 < x1 ? x1 : x0;
-          x0 = lo2;
-        } else {
-          const unsigned long long y0 = __shfl_xor_sync(0xffffffffu, x0, j);
-          const unsigned long long y1 = __shfl_xor_sync(0xffffffffu, x1, j);
-          const bool lower = (lane & j) == 0;
-          const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
-          x0 = (lower == up0) ? (x0 < y0 ? x0 : y0) : (x0 < y0 ? y0 : x0);
-          x1 = (lower == up1) ? (x1 < y1 ? x1 : y1) : (x1 < y1 ? y1 : x1);
-        }
-      }
-    }
-    S.key[lane] = x0;
-    if (lane + 32 < n) S.key[lane + 32] = x1;
-  } else {
-    for (int i = n + lane; i < np2; i += 32) S.key[i] = ~0ull;
-    __syncwarp();
-    for (int k = 2; k <= np2; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < np2; i += 32) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const unsigned long long a = S.key[i], c = S.key[ixj];
-            if ((a > c) == ((i & k) == 0)) {
-              S.key[i] = c;
-              S.key[ixj] = a;
-            }
-          }
-        }
-        __syncwarp();
-      }
-    }
-  }
+  warp_sort_keys(S.key, n, lane);
   __syncwarp();
   // pass 2: the row table in EDF order (32 rows at a time, prefix of max q by warp scan)
   long long qsum = 0, wt = 0, wr = 0;

@@ -29,6 +29,7 @@ struct Req {
 struct Server {
   int64_t now = 0, busy_until = NEVER;
   int64_t plan_until = 0;  // cost model: no stage starts before the plan is ready
+  int64_t plan_carry = 0;  // table cells not yet charged (planning time accrues in whole ticks)
   int running = -1;  // index into reqs of the stage in flight
   bool dirty = false;
   int rr_last = -1;
@@ -352,7 +353,9 @@ extern "C" int ic_sim_run_dump(const ic_sim_config* cfg, ic_sim_result* out, ic_
     for (int64_t b = 0; b < B; ++b) {
       Server& v = S.sv[need[b]];
       if (c.plan_cells_per_tick > 0) {  // the plan holds the server before the next stage
-        const int64_t cost = (cells[b] + c.plan_cells_per_tick - 1) / c.plan_cells_per_tick;
+        v.plan_carry += cells[b];
+        const int64_t cost = v.plan_carry / c.plan_cells_per_tick;
+        v.plan_carry -= cost * c.plan_cells_per_tick;
         v.plan_until = v.now + cost;
         S.plan_ticks += cost;
       }
