@@ -199,11 +199,20 @@ __global__ void __launch_bounds__(256, 4) reassign_kernel(const __grid_constant_
         F = __shfl_sync(0xffffffffu, f, 31);
       }
       __syncwarp();
-      if (norel && lane == 0) {  // suffix minimum slack of the truncated schedule (reuses ord)
-        long long smin = 1ll << 40;
-        for (int pos = n - 1; pos >= 0; --pos) {
-          ord[pos] = (int)min(smin, (long long)(1 << 30));
-          if (ck[pos] >= 0) smin = min(smin, (long long)dd[pos] - (fb[pos] + ck[pos]));
+      if (norel) {  // suffix minimum slack of the truncated schedule after each position (reuses ord)
+        int carry = 1 << 30;  // min over the positions of the later chunks
+        for (int base0 = (n - 1) & ~31; base0 >= 0; base0 -= 32) {
+          const int pos = base0 + lane;
+          int sl = pos < n && ck[pos] >= 0 ? (int)min((long long)dd[pos] - (fb[pos] + ck[pos]), 1ll << 30) : 1 << 30;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {  // inclusive suffix minimum within the chunk
+            const int y = __shfl_down_sync(0xffffffffu, sl, o);
+            if (lane + o < 32) sl = min(sl, y);
+          }
+          int after = __shfl_down_sync(0xffffffffu, sl, 1);  // positions strictly after pos
+          if (lane == 31) after = 1 << 30;
+          if (pos < n) ord[pos] = min(after, carry);
+          carry = min(carry, __shfl_sync(0xffffffffu, sl, 0));
         }
       }
       __syncwarp();
