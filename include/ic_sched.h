@@ -189,8 +189,18 @@ int ic_sched_reassign_batch(ic_sched* h, const ic_batch_in* in, const ic_stage_u
  *                                     state, the rest recomputed; the state is updated, so
  *                                     arrivals can be chained.  Results are identical to a
  *                                     full ic_sched_solve_batch of the new instances.
- * Requires a fixed Delta (delta_micro > 0: the FPTAS step eps*R/N changes with N) and
- * max_horizon <= 16384 (IC_ERR_INVALID_ARG / IC_ERR_LIMIT otherwise).  Every ckpt-th row
+ *   ic_sched_depart_batch(...)        a departure (a request answered or expired
+ *                                     leaves the task set): the inputs are the previous
+ *                                     instances with ONE task removed (the others unchanged
+ *                                     and in the same order); removed_index[b] is its input
+ *                                     index in the previous instance and removed_deadline[b],
+ *                                     removed_release[b] its deadline and release, which fix
+ *                                     its old EDF position k: rows before k are kept, the rest
+ *                                     recomputed, the state updated.  Results are identical to
+ *                                     a full solve of the new instances.  Device pointers [B].
+ * Requires a fixed Delta (delta_micro > 0: the FPTAS step eps*R/N changes with N)
+ * (IC_ERR_INVALID_ARG otherwise); any horizon (in-place rows at H = 32768 included; the state
+ * then holds (max_tasks / ckpt + 1) * (H + 1) * 4 bytes of rows per instance).  Every ckpt-th row
  * is kept (ic_sched_tuning.ckpt, default 4), so a re-plan restarts at the last kept row before the
  * arrival; if the instance's sweep axis changes (time vs reward) it restarts at row 0.
  * Same stream/ownership rules as ic_sched_solve_batch. */
@@ -198,6 +208,9 @@ int64_t ic_sched_state_bytes(const ic_sched* h, int64_t n_instances);
 int ic_sched_solve_batch_state(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* state,
                                void* cuda_stream);
 int ic_sched_replan_batch(ic_sched* h, const ic_batch_in* in, void* state, ic_batch_out* out, void* cuda_stream);
+int ic_sched_depart_batch(ic_sched* h, const ic_batch_in* in, const int32_t* removed_index,
+                          const int32_t* removed_deadline, const int32_t* removed_release, void* state,
+                          ic_batch_out* out, void* cuda_stream);
 
 /* Launch geometry chosen at create time (for tests, bench and profiling).  The fields describe
  * the kernel plain solves run first (the one-warp-per-instance kernel for H <= 1024 rows or

@@ -92,7 +92,7 @@ class _GenCfg(ctypes.Structure):
 
 EXPORTED = ("ic_sched_create", "ic_sched_create_tuned", "ic_sched_solve_batch", "ic_sched_solve_batch_host", "ic_sched_destroy",
             "ic_sched_get_info", "ic_gen_batch_device", "ic_sched_reassign_batch", "ic_sched_state_bytes",
-            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sim_run", "ic_sim_run_dump",
+            "ic_sched_solve_batch_state", "ic_sched_replan_batch", "ic_sched_depart_batch", "ic_sim_run", "ic_sim_run_dump",
             "ic_probe_smem")
 
 IC_UTIL_GIVEN, IC_UTIL_MAX, IC_UTIL_EXP, IC_UTIL_LIN = 0, 1, 2, 3
@@ -227,6 +227,8 @@ def load_library():
         lib.ic_sched_solve_batch_state.argtypes = [ctypes.c_void_p, P(_In), P(_Out), ctypes.c_void_p,
                                                    ctypes.c_void_p]
         lib.ic_sched_replan_batch.argtypes = [ctypes.c_void_p, P(_In), ctypes.c_void_p, P(_Out), ctypes.c_void_p]
+        lib.ic_sched_depart_batch.argtypes = [ctypes.c_void_p, P(_In)] + [ctypes.c_void_p] * 4 + \
+            [P(_Out), ctypes.c_void_p]
         lib.ic_sched_state_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         lib.ic_sim_run.argtypes = [P(SimConfig), P(SimResult)]
         lib.ic_sim_run_dump.argtypes = [P(SimConfig), P(SimResult), P(_SimDump)]
@@ -400,6 +402,27 @@ class Scheduler:
     def replan_batch(self, inputs: dict, state, outputs: dict | None = None, stream=None) -> dict:
         """ic_sched_replan_batch: each instance gained one task (appended last); re-plan from its row."""
         return self._state_call("ic_sched_replan_batch", inputs, state, outputs, stream)
+
+    def depart_batch(self, inputs: dict, removed_index, removed_deadline, removed_release, state,
+                     outputs: dict | None = None, stream=None) -> dict:
+        """ic_sched_depart_batch: each instance lost one task (its previous input index, deadline
+        and release given per instance as int32 CUDA tensors); re-plan from its old EDF row."""
+        import torch
+        if outputs is None:
+            outputs = alloc_outputs(_n_instances(inputs), inputs["release"].numel(),
+                                    device=inputs["release"].device)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        for x in (removed_index, removed_deadline, removed_release):
+            if x.dtype != torch.int32 or not x.is_contiguous() or x.numel() < _n_instances(inputs):
+                raise ValueError("removed_* must be contiguous int32 tensors with one entry per instance")
+        i, o = self._marshal(inputs, outputs)
+        rc = self._lib.ic_sched_depart_batch(self._h, ctypes.byref(i), _ptr(removed_index), _ptr(removed_deadline),
+                                             _ptr(removed_release), _ptr(state), ctypes.byref(o),
+                                             ctypes.c_void_p(stream.cuda_stream))
+        if rc != IC_OK:
+            raise ICSchedError("ic_sched_depart_batch", rc)
+        return outputs
 
     def _state_call(self, fn, inputs, state, outputs, stream):
         import torch

@@ -401,8 +401,11 @@ static int64_t state_stride(const ic_sched* h) {
   return (state_rows_bytes(h) + state_dec_bytes(h) + (int64_t)(h->cfg.max_tasks + 1) * 4 + 255) & ~(int64_t)255;
 }
 
+struct Departure {
+  const int32_t *index, *deadline, *release;
+};
 static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream, void* state,
-                        int replan);
+                        int replan, const Departure* dep = nullptr);
 
 extern "C" int ic_sched_solve_batch(ic_sched* h, const ic_batch_in* in, ic_batch_out* out,
                                     void* cuda_stream) {
@@ -417,7 +420,6 @@ extern "C" int64_t ic_sched_state_bytes(const ic_sched* h, int64_t n_instances) 
 static int state_ok(const ic_sched* h, const void* state) {
   if (!h || !state) return IC_ERR_INVALID_ARG;
   if (h->cfg.delta_micro == 0) return IC_ERR_INVALID_ARG;  // FPTAS Delta changes with every arrival
-  if (h->sb) return IC_ERR_LIMIT;                          // in-place rows (H > 16384) keep no state
   return IC_OK;
 }
 
@@ -433,8 +435,19 @@ extern "C" int ic_sched_replan_batch(ic_sched* h, const ic_batch_in* in, void* s
   return rc != IC_OK ? rc : launch_solve(h, in, out, cuda_stream, state, 1);
 }
 
+extern "C" int ic_sched_depart_batch(ic_sched* h, const ic_batch_in* in, const int32_t* removed_index,
+                                     const int32_t* removed_deadline, const int32_t* removed_release, void* state,
+                                     ic_batch_out* out, void* cuda_stream) {
+  const int rc = state_ok(h, state);
+  if (rc != IC_OK) return rc;
+  if (!in || (in->n_instances > 0 && (!removed_index || !removed_deadline || !removed_release)))
+    return IC_ERR_INVALID_ARG;
+  const Departure dep{removed_index, removed_deadline, removed_release};
+  return launch_solve(h, in, out, cuda_stream, state, 1, &dep);
+}
+
 static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, void* cuda_stream, void* state,
-                        int replan) {
+                        int replan, const Departure* dep) {
   if (!h) return IC_ERR_INVALID_ARG;
   int rc = check_io(in, out);
   if (rc != IC_OK) return rc;
@@ -498,6 +511,11 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.state_dec_off = state_rows_bytes(h);
   p.state_tail_off = state_rows_bytes(h) + state_dec_bytes(h);
   p.replan = replan;
+  if (dep) {
+    p.dep_index = dep->index;
+    p.dep_deadline = dep->deadline;
+    p.dep_release = dep->release;
+  }
   p.ckpt = h->ckpt;
   p.work = h->work;
   p.ndec = L.ndec;
@@ -507,7 +525,7 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
                ((uintptr_t)p.opt_gain & 15) == 0 && !h->no_vec_loads;
   const Params pw = p;  // the warp-specialised kernel's parameters
-  if (h->solo_fn && !state) {  // one warp per instance (ic_solo_kernel.cuh)
+  if (h->solo_fn && (!state || !h->hybrid)) {  // one warp per instance (ic_solo_kernel.cuh)
     const Layout& S = h->SL;
     if (h->hybrid) {  // room for every id the solo kernel may defer, and a zeroed count
       if (in->n_instances > h->defer_cap) {

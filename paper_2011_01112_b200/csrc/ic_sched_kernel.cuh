@@ -85,7 +85,8 @@ struct Params {
   // columns and tail value, stride H+1), the decisions and the tail nibbles
   char* state;
   int64_t state_stride, state_dec_off, state_tail_off;
-  int replan;  // 1: the last task of each instance is a new arrival; rows before it are kept
+  int replan;  // 1: re-plan from the changed row (an arrival appended last, or a departure)
+  const int32_t *dep_index, *dep_deadline, *dep_release;  // departures: the removed task per instance
   int ckpt;    // rows kept in the state: every ckpt-th (rows ckpt-1, 2 ckpt-1, ...), power of two
   unsigned long long* work;  // [2] dynamic instance counter, CTAs finished (reset by the last CTA)
   // hybrid solves (fixed Delta, long horizon): the solo kernel runs the instances whose sweep
@@ -653,15 +654,27 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     mi[9] = rw ? 1 : 0;
     mi[10] = 0;
   }
-  if (p.replan) {  // the arrival is the instance's last task: rows before its EDF position stand
+  if (p.replan) {  // rows before the changed EDF position stand (Alg. 1 from row k)
     int k = 0;
-    for (int pos = lane; pos < n; pos += 32)
-      if ((int)(S.key[pos] & 0xFFF) == n - 1) k = pos;
-    k = __reduce_max_sync(0xffffffffu, k);
+    if (p.dep_index) {
+      // departure: the removed task j (input index in the previous instance, whose other tasks
+      // keep their order) sat after exactly the remaining tasks that precede it in (d, r, index)
+      const int j = p.dep_index[b], dj = p.dep_deadline[b], rj = min(max(p.dep_release[b], 0), (1 << 20) - 1);
+      for (int i = lane; i < n; i += 32) {
+        const int di = S.sd[i], ri = min(max(S.sr[i], 0), (1 << 20) - 1);
+        k += (di < dj) || (di == dj && (ri < rj || (ri == rj && i < j)));
+      }
+      k = (int)__reduce_add_sync(0xffffffffu, (unsigned)k);
+    } else {  // arrival: the instance's last task
+      for (int pos = lane; pos < n; pos += 32)
+        if ((int)(S.key[pos] & 0xFFF) == n - 1) k = pos;
+      k = __reduce_max_sync(0xffffffffu, k);
+    }
     k = k / p.ckpt * p.ckpt;  // restart after the last checkpointed row before the arrival
     const int32_t* st = state_tail(p, b);
     if (st[p.max_tasks] != (rw ? 1 : 0)) k = 0;  // the sweep axis changed: nothing to reuse
-    for (int pos = lane; pos < k; pos += 32) S.tail[s * p.max_tasks + pos] = st[pos];
+    if (S.tail)
+      for (int pos = lane; pos < k; pos += 32) S.tail[s * p.max_tasks + pos] = st[pos];
     if (lane == 0) S.misc[s * 16 + 10] = k;
   }
   __syncwarp();

@@ -70,12 +70,21 @@ static __device__ __noinline__ int solo_setup(const Params& p, unsigned char* ba
 // a4 + a5: the rows in place, then the optimum of row N into misc[5], misc[6].
 template <bool DROP>
 __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
+  // (dec: the warp's decision slab; replaced by the instance's state when one is kept)
   int32_t* const rowbuf = (int32_t*)(base + p.off_rowbuf);
   int32_t* const buf = rowbuf + p.pad;
   long long* mi = (long long*)(base + p.off_misc);
   const int n = (int)mi[0];
   const bool rw = mi[9] != 0;
   const int d_first = (int)mi[7], dl = (int)mi[8];
+  // NEXT-2 (re-plan state): decisions go to the caller's state, every ckpt-th row is kept
+  const int64_t bcur = mi[2];
+  const bool keep_state = p.state != nullptr;
+  const int k0 = p.replan ? (int)mi[10] : 0;  // first row to (re)compute
+  if (keep_state) {
+    dec = state_dec(p, bcur);
+    if (lane == 0) state_tail(p, bcur)[p.max_tasks] = rw ? 1 : 0;
+  }
   const bool refill = (int)rw != (int)mi[12];
   __syncwarp();
   if (refill) {  // the pad left of column 0 reads as "invalid" on this axis
@@ -90,19 +99,32 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
   __syncwarp();
   const int4* inf = (const int4*)(base + p.off_info);
   const int32_t* aux = (const int32_t*)(base + p.off_aux);
-  const int2* ops = (const int2*)(base + p.off_rowp);
-  uint32_t* decrow = dec;
   const int kp = p.kp;
   const int dec_row_words = p.nq * 32;
+  const int2* ops = (const int2*)(base + p.off_rowp) + k0 * kp;
+  uint32_t* decrow = dec + (size_t)k0 * dec_row_words;
   int M = 15;
+  if (k0 > 0) {  // restore row k0-1 (its active columns, then its tail value up to d_k0)
+    const int32_t* srow = state_rows(p, bcur) + (int64_t)(k0 / p.ckpt - 1) * (p.H + 1);
+    const int dprev = inf[k0 - 1].x, dk = inf[k0].x;  // deadlines, or Qpre on the reward axis
+    M = srow[p.H];
+    for (int t = lane; t <= dprev; t += 32) buf[t] = srow[t];
+    const int first = dprev + 1 > 0 ? dprev + 1 : 0;
+    for (int t = first + lane; t <= dk; t += 32) buf[t] = rw ? INFV : M;
+    __syncwarp();
+  }
 #pragma unroll 1
-  for (int pos = 0; pos < n; ++pos) {
+  for (int pos = k0; pos < n; ++pos) {
     const int4 f = inf[pos];
     const int d = f.x, K = f.y & 255;
     if (rw) {
       // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
       dp_row_dispatch<1, true, DROP, true, IC_SOLO_KC>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
       __syncwarp();
+      if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
+        int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * (p.H + 1);
+        for (int t = lane; t <= d; t += 32) srow[t] = buf[t];
+      }
     } else {
       dp_row_dispatch<1, true, DROP, false, IC_SOLO_KC>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
       __syncwarp();
@@ -111,6 +133,11 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
         M = buf[d];
       else if (!DROP)
         M = NEG | 15;
+      if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint: active columns and tail value
+        int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * (p.H + 1);
+        for (int t = lane; t <= d; t += 32) srow[t] = buf[t];
+        if (lane == 0) srow[p.H] = M;
+      }
       const int dn = f.w;
       const int first = d + 1 > 0 ? d + 1 : 0;
 #pragma unroll 1

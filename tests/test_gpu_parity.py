@@ -417,3 +417,85 @@ def test_hybrid_reward_rows(mode):
     assert got["_info"]["hybrid"] == 1 and got["_info"]["kernels_per_solve"] == 2
     assert_parity(got, ref, f"hybrid mode={mode}")
     np.testing.assert_array_equal(got["stats"], stats_from(got, batch))
+
+
+def _remove_one(batch, rng):
+    """Per instance, remove one random task (the others keep their order); returns the reduced
+    batch and the removed task's previous input index, deadline and release."""
+    from gen import Batch
+    parts, idx, dl, rl = [], [], [], []
+    for b in range(batch.n_instances):
+        one = batch.instance(b)
+        n = one.n_total_tasks
+        j = int(rng.integers(0, n))
+        keep = np.array([i for i in range(n) if i != j], np.int64)
+        parts.append(Batch(np.array([0, n - 1], np.int64), one.release[keep], one.deadline[keep],
+                           one.mand_wcet[keep], one.n_opt[keep], one.opt_wcet[keep], one.mand_conf[keep],
+                           one.opt_gain[keep]))
+        idx.append(j)
+        dl.append(int(one.deadline[j]))
+        rl.append(int(one.release[j]))
+    cat = gen.concat(parts, batch.opt_stride)
+    to = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")
+    return cat, to(idx), to(dl), to(rl)
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("shape", ["C2", "tiny", "H32768"])
+def test_departures_and_arrivals(kernel, mode, shape):
+    """NEXT-2 both ways (P:L112 arrivals, P:L236 departures): chained departures and arrivals
+    re-planned from the state equal full solves of the changed task sets, for the solo and the
+    warp-specialised kernels, and with in-place rows at H = 32768."""
+    import paper_2011_01112_b200 as pkg
+    from tests.gpu_util import to_device
+    rng = np.random.default_rng(200 + mode + 10 * kernel)
+    if shape == "C2":
+        full = gen.generate("C2", 300)
+        mt, mo, H = 32, 4, 1024
+    elif shape == "tiny":
+        full = gen.tiny_random(rng, 1500, max_tasks=7, max_opt=3, horizon=40)
+        mt, mo, H = 7, 3, 40
+    else:
+        full = gen.tiny_random(rng, 200, max_tasks=8, max_opt=3, horizon=32768, p_release=0.3)
+        full.mand_wcet[:] = full.mand_wcet * 900
+        full.opt_wcet[:] = full.opt_wcet * 700
+        mt, mo, H = 8, 3, 32768
+    full = full.select(np.nonzero(np.diff(full.task_begin) >= 4)[0])
+    sc = pkg.SchedConfig(max_tasks=mt, max_opt_stages=mo, max_horizon=H, delta_micro=100_000, drop_mode=mode)
+    ocfg = OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=mt, max_horizon=H)
+    with pkg.Scheduler(sc, dict(kernel=kernel, ckpt=2)) as s:
+        state = torch.zeros(s.state_bytes(full.n_instances), dtype=torch.uint8, device="cuda")
+        s.solve_batch_state(to_device(full), state)
+        cur = full
+        for step in range(3):
+            cur, j, dl, rl = _remove_one(cur, rng)
+            out = s.depart_batch(to_device(cur), j, dl, rl, state)
+            torch.cuda.synchronize()
+            got = {k: v.cpu().numpy() for k, v in out.items()}
+            assert_parity(got, oracle.solve(cur, ocfg, TIME), f"{shape} departure {step} mode={mode} k={kernel}")
+        # an arrival after the departures: the full instance's last task is appended again
+        parts = [gen.concat([cur.instance(b), _last_task(full.instance(b))], mo) for b in range(cur.n_instances)]
+        grown = _merge_tasks(parts, mo)
+        out = s.replan_batch(to_device(grown), state)
+        torch.cuda.synchronize()
+        got = {k: v.cpu().numpy() for k, v in out.items()}
+        assert_parity(got, oracle.solve(grown, ocfg, TIME), f"{shape} arrival after departures mode={mode}")
+
+
+def _last_task(one):
+    from gen import Batch
+    n = one.n_total_tasks
+    return Batch(np.array([0, 1], np.int64), one.release[n - 1:], one.deadline[n - 1:], one.mand_wcet[n - 1:],
+                 one.n_opt[n - 1:], one.opt_wcet[n - 1:], one.mand_conf[n - 1:], one.opt_gain[n - 1:])
+
+
+def _merge_tasks(parts, stride):
+    """Each part is a two-instance batch (the current tasks, one new task): one instance each."""
+    from gen import Batch
+    out = []
+    for p in parts:
+        T = p.n_total_tasks
+        out.append(Batch(np.array([0, T], np.int64), p.release, p.deadline, p.mand_wcet, p.n_opt, p.opt_wcet,
+                         p.mand_conf, p.opt_gain))
+    return gen.concat(out, stride)
