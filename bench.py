@@ -306,17 +306,38 @@ def run_reference(args, cw, rank, world):
 
 
 def run_replan(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong):
-    """--op replan: every instance's last task arrives; the rows before its EDF position come from
-    the state of the solve without it (Alg. 1 from row k).  Reported beside a full solve."""
+    """--op replan: NEXT-2, Alg. 1 from row k.  Arrival: every instance's last task
+    arrives and the rows before its EDF position come from the state of the solve without it.
+    Departure: every instance loses one task (index b*7 mod N) and the rows before its
+    old EDF position come from the state of the solve with it.  Both reported beside a full solve
+    of the same instances (the state-keeping solve itself is not timed)."""
     import torch
-    import torch.distributed as dist
     N = cw.n_tasks
-    base = {k: (v.view(n_inst, N, -1)[:, :N - 1].reshape(n_inst * (N - 1), -1).squeeze(-1).contiguous()
-                if k != "task_begin" else torch.arange(n_inst + 1, device=dev, dtype=torch.int64) * (N - 1))
-            for k, v in inputs.items()}
-    base["opt_wcet"] = base["opt_wcet"].view(-1, cw.n_opt)
-    base["opt_gain"] = base["opt_gain"].view(-1, cw.n_opt)
+    pkg = sys.modules["paper_2011_01112_b200"]
+
+    def subset(drop):  # every instance without task drop[b] (others in order)
+        keep = torch.ones(n_inst, N, dtype=torch.bool, device=dev)
+        keep[torch.arange(n_inst, device=dev), drop] = False
+        sub = {}
+        for k, v in inputs.items():
+            if k == "task_begin":
+                sub[k] = torch.arange(n_inst + 1, device=dev, dtype=torch.int64) * (N - 1)
+            else:
+                w = v.view(torch.int32) if v.dtype == torch.uint32 else v  # no uint32 gather on CUDA
+                w = (w.view(n_inst, N, -1)[keep].reshape(n_inst * (N - 1), -1) if v.dim() == 2
+                     else w.view(n_inst, N)[keep]).contiguous()
+                sub[k] = w.view(torch.uint32) if v.dtype == torch.uint32 else w
+        return sub
+
+    last = torch.full((n_inst,), N - 1, dtype=torch.long, device=dev)
+    base = subset(last)  # before the arrival
+    dropj = (torch.arange(n_inst, device=dev) * 7) % N
+    after = subset(dropj)  # after the departure
+    j32 = dropj.to(torch.int32)
+    dl = inputs["deadline"].view(n_inst, N)[torch.arange(n_inst, device=dev), dropj].to(torch.int32).contiguous()
+    rl = inputs["release"].view(n_inst, N)[torch.arange(n_inst, device=dev), dropj].to(torch.int32).contiguous()
     state = torch.empty(sched.state_bytes(n_inst), dtype=torch.uint8, device=dev)
+    out2 = pkg.alloc_outputs(n_inst, n_inst * (N - 1), device=dev)
     k = args.steps or 10
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     with torch.cuda.stream(stream):
@@ -326,26 +347,37 @@ def run_replan(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, s
         for _ in range(k):
             sched.solve_batch(inputs, out, stream)
         ev[1].record(stream)
-        tr = 0.0
+        ta = td = 0.0
         for _ in range(k):
             sched.solve_batch_state(base, state, None, stream)
             ev[2].record(stream)
             sched.replan_batch(inputs, state, out, stream)
             ev[3].record(stream)
             ev[3].synchronize()
-            tr += ev[2].elapsed_time(ev[3])
+            ta += ev[2].elapsed_time(ev[3])
+        for _ in range(k):
+            sched.solve_batch_state(inputs, state, None, stream)
+            ev[2].record(stream)
+            sched.depart_batch(after, j32, dl, rl, state, out2, stream)
+            ev[3].record(stream)
+            ev[3].synchronize()
+            td += ev[2].elapsed_time(ev[3])
     stream.synchronize()
     full_ms = ev[0].elapsed_time(ev[1]) / k
-    rep_ms = tr / k
+    rep_ms, dep_ms = ta / k, td / k
     if rank == 0:
         total = n_inst * world
+        info = sched.info()
         print(json.dumps({
             "metric": "re-plans on arrival/sec (Alg. 1 from row k)", "value": total / (rep_ms / 1e3),
             "unit": "instances/s", "n_gpus": world, "steps": k, "warmup": args.warmup, "ms_per_step": rep_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (device-generated, seeded)", "config": workload_config(cw, args, n_inst),
-            "full_solve_ms": full_ms, "speedup_vs_full_solve": full_ms / rep_ms, "gpu_launches": 2 * k}),
-            flush=True)
+            "full_solve_ms": full_ms, "speedup_vs_full_solve": full_ms / rep_ms,
+            "departure": {"value": total / (dep_ms / 1e3), "unit": "instances/s", "ms_per_step": dep_ms,
+                          "speedup_vs_full_solve": full_ms / dep_ms},
+            "kernel": info, "state_bytes_per_instance": sched.state_bytes(1),
+            "gpu_launches": 3 * k * info.get("kernels_per_solve", 1)}), flush=True)
 
 
 def run_reassign(args, cw, sched, inputs, out, stream, n_inst, world, rank, dev, strong):

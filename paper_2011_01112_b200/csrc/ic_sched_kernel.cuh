@@ -670,7 +670,8 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
         if ((int)(S.key[pos] & 0xFFF) == n - 1) k = pos;
       k = __reduce_max_sync(0xffffffffu, k);
     }
-    k = k / p.ckpt * p.ckpt;  // restart after the last checkpointed row before the arrival
+    k = min(k, n - 1);        // a departure past the last row still recomputes the last row
+    k = k / p.ckpt * p.ckpt;  // restart after the last checkpointed row before the change
     const int32_t* st = state_tail(p, b);
     if (st[p.max_tasks] != (rw ? 1 : 0)) k = 0;  // the sweep axis changed: nothing to reuse
     if (S.tail)
