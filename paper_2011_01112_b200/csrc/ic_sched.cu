@@ -511,6 +511,7 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.state_dec_off = state_rows_bytes(h);
   p.state_tail_off = state_rows_bytes(h) + state_dec_bytes(h);
   p.replan = replan;
+  p.nw = h->nw;
   if (dep) {
     p.dep_index = dep->index;
     p.dep_deadline = dep->deadline;

@@ -79,7 +79,8 @@ struct Params {
   int nslots;  // 2: set up instance b+1 while the DP sweeps b; 1: serialised (large N)
   int cap;     // row buffer capacity in columns (32 NW x COLS)
   int off_aux, off_sQ;
-  int solo_warp_bytes;  // solo kernel: shared-memory bytes of one warp's private region
+  int solo_warp_bytes;  // solo kernel: shared-memory bytes of one warp's private region (0: ws kernel)
+  int nw;               // DP warps of the warp-specialised kernel
   int axis_mode;  // 0 auto (per instance), 1 time axis only, 2 reward axis whenever eligible
   // NEXT-2 (incremental re-plan): per-instance state = every DP row (its active
   // columns and tail value, stride H+1), the decisions and the tail nibbles
@@ -677,6 +678,16 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     if (S.tail)
       for (int pos = lane; pos < k; pos += 32) S.tail[s * p.max_tasks + pos] = st[pos];
     if (lane == 0) S.misc[s * 16 + 10] = k;
+    // the backtrack will walk the kept rows' decisions (written by an earlier call, likely
+    // evicted to HBM): pull their lines into L2 now so they arrive while the rows >= k sweep
+    const int NTs = p.solo_warp_bytes ? 32 : 32 * p.nw;
+    const char* db = (const char*)state_dec(p, b);
+    for (int pos = lane; pos < k; pos += 32) {
+      const int cols = S.info[s * p.max_tasks + pos].x + 1;
+      const int lines = cols > 0 ? (((cols - 1) / NTs) / 8 + 1) * (NTs / 32) : 0;
+      const char* row = db + (int64_t)pos * p.nq * NTs * 4;
+      for (int l = 0; l < lines; ++l) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(row + l * 128));
+    }
   }
   __syncwarp();
   return ST_OK;
