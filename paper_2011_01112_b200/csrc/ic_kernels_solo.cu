@@ -2,5 +2,8 @@
 #include "ic_solo_kernel.cuh"
 
 namespace icsched {
-KernelFn kernel_solo(bool drop) { return drop ? ic_solo_kernel<true> : ic_solo_kernel<false>; }
+KernelFn kernel_solo(bool drop, bool state) {
+  if (state) return drop ? ic_solo_kernel<true, true> : ic_solo_kernel<false, true>;
+  return drop ? ic_solo_kernel<true, false> : ic_solo_kernel<false, false>;
+}
 }  // namespace icsched

@@ -140,7 +140,7 @@ struct ic_sched {
   int64_t tb_cap;
   // solo kernel (one warp per instance) for plain solves when chosen; the state / re-plan
   // entry points always use the warp-specialised kernel above
-  KernelFn solo_fn;
+  KernelFn solo_fn, solo_state_fn;  // plain solves / the re-plan state entry points
   int hybrid;                 // 1: the solo kernel's row holds the reward axis only (fixed Delta,
                               // long horizon); instances it cannot sweep go to the ws kernel
   int64_t* defer_ids;         // [defer_cap] ids the solo kernel deferred; defer_n = their count
@@ -301,11 +301,13 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
     const int spad = tu.pad_cols ? ((tu.pad_cols + 31) & ~31) : 64 > c.max_horizon ? ((c.max_horizon + 31) & ~31) : 64;
     Layout S = make_solo_layout(c, spad, hybrid ? (int)qcap : 0);
     h->hybrid = hybrid ? 1 : 0;
-    KernelFn sf = icsched::kernel_solo(drop);
+    KernelFn sf = icsched::kernel_solo(drop, false);
+    KernelFn sfs = icsched::kernel_solo(drop, true);
     const int bytes = S.bytes * IC_SOLO_WPC;
     int sp = 0;
     if (bytes > kSmemLimit) rc = IC_ERR_LIMIT;
-    if (rc == IC_OK && cudaFuncSetAttribute(sf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) != cudaSuccess)
+    if (rc == IC_OK && (cudaFuncSetAttribute(sf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) != cudaSuccess ||
+                        cudaFuncSetAttribute(sfs, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) != cudaSuccess))
       rc = IC_ERR_CUDA;
     if (rc == IC_OK &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sp, sf, 32 * IC_SOLO_WPC, bytes) != cudaSuccess)
@@ -314,6 +316,7 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
     if (rc == IC_OK && tu.ctas_per_sm && tu.ctas_per_sm < sp) sp = tu.ctas_per_sm;
     if (rc == IC_OK) {
       h->solo_fn = sf;
+      h->solo_state_fn = sfs;
       h->SL = S;
       h->solo_ctas_per_sm = sp;
       h->solo_grid = sms * sp;
@@ -571,7 +574,8 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
     int64_t grid = h->solo_grid;
     const int64_t need = (in->n_instances + IC_SOLO_WPC - 1) / IC_SOLO_WPC;
     if (grid > need) grid = need;
-    h->solo_fn<<<(unsigned)grid, 32 * IC_SOLO_WPC, S.bytes * IC_SOLO_WPC, (cudaStream_t)cuda_stream>>>(p);
+    (state ? h->solo_state_fn : h->solo_fn)<<<(unsigned)grid, 32 * IC_SOLO_WPC, S.bytes * IC_SOLO_WPC,
+                                               (cudaStream_t)cuda_stream>>>(p);
     if (cudaGetLastError() != cudaSuccess) return IC_ERR_CUDA;
     if (!h->hybrid) return IC_OK;
     // the deferred instances: the warp-specialised kernel over the listed ids (its CTAs

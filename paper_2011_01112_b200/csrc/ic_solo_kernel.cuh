@@ -68,7 +68,7 @@ static __device__ __noinline__ int solo_setup(const Params& p, unsigned char* ba
 }
 
 // a4 + a5: the rows in place, then the optimum of row N into misc[5], misc[6].
-template <bool DROP>
+template <bool DROP, bool STATE>
 __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
   // (dec: the warp's decision slab; replaced by the instance's state when one is kept)
   int32_t* const rowbuf = (int32_t*)(base + p.off_rowbuf);
@@ -79,9 +79,8 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
   const int d_first = (int)mi[7], dl = (int)mi[8];
   // NEXT-2 (re-plan state): decisions go to the caller's state, every ckpt-th row is kept
   const int64_t bcur = mi[2];
-  const bool keep_state = p.state != nullptr;
-  const int k0 = p.replan ? (int)mi[10] : 0;  // first row to (re)compute
-  if (keep_state) {
+  const int k0 = STATE && p.replan ? (int)mi[10] : 0;  // first row to (re)compute
+  if (STATE) {
     dec = state_dec(p, bcur);
     if (lane == 0) state_tail(p, bcur)[p.max_tasks] = rw ? 1 : 0;
   }
@@ -104,7 +103,7 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
   const int2* ops = (const int2*)(base + p.off_rowp) + k0 * kp;
   uint32_t* decrow = dec + (size_t)k0 * dec_row_words;
   int M = 15;
-  if (k0 > 0) {  // restore row k0-1 (its active columns, then its tail value up to d_k0)
+  if (STATE && k0 > 0) {  // restore row k0-1 (its active columns, then its tail value up to d_k0)
     const int32_t* srow = state_rows(p, bcur) + (int64_t)(k0 / p.ckpt - 1) * (p.H + 1);
     const int dprev = inf[k0 - 1].x, dk = inf[k0].x;  // deadlines, or Qpre on the reward axis
     M = srow[p.H];
@@ -121,7 +120,7 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
       // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
       dp_row_dispatch<1, true, DROP, true, IC_SOLO_KC>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
       __syncwarp();
-      if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
+      if (STATE && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
         int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * (p.H + 1);
         for (int t = lane; t <= d; t += 32) srow[t] = buf[t];
       }
@@ -133,7 +132,7 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
         M = buf[d];
       else if (!DROP)
         M = NEG | 15;
-      if (p.state && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint: active columns and tail value
+      if (STATE && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint: active columns and tail value
         int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * (p.H + 1);
         for (int t = lane; t <= d; t += 32) srow[t] = buf[t];
         if (lane == 0) srow[p.H] = M;
@@ -193,7 +192,9 @@ static __device__ __noinline__ void solo_finish(const Params& p, unsigned char* 
   tail_outputs<1>(p, S, 0, lane, solo_acc(p, base));
 }
 
-template <bool DROP>
+// STATE: the re-plan entry points (decisions and checkpoint rows kept in the caller's state);
+// plain solves run the variant without any of that code.
+template <bool DROP, bool STATE>
 __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
       b = (int64_t)__shfl_sync(0xffffffffu, v, 0);
     } while (b < p.B && solo_setup(p, base, b, lane) != ST_OK);
     if (b >= p.B) break;
-    solo_sweep<DROP>(p, base, dec, lane);
+    solo_sweep<DROP, STATE>(p, base, dec, lane);
     solo_finish(p, base, dec, lane);
   }
   __syncwarp();
@@ -225,6 +226,6 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
   }
 }
 
-KernelFn kernel_solo(bool drop);
+KernelFn kernel_solo(bool drop, bool state);
 
 }  // namespace icsched
