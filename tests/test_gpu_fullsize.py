@@ -8,7 +8,7 @@ with ONE ic_sched_solve_batch exactly as bench.py does, and then
   * checks properties that hold at any size over EVERY instance of the launch: kept tasks
     meet their deadlines and run back to back in EDF order, finish = start +
     C_i(kept), makespan / confidence / stats recomputed from the plan.
-Sample sizes follow BASELINE.md §3 "Parity coverage": C2 in full, C3 1-in-16, C4 1-in-4,
+Sample sizes follow BASELINE.md §3 "Parity coverage": C2 and C4 in full, C3 1-in-16,
 C5 1-in-64 (runs of 64 consecutive ids, one per 4096-id window, so every U block and the
 highest task-row offsets — beyond 2^31 words of opt_wcet — are covered).
 """
@@ -137,7 +137,7 @@ def test_c5_full_launch_one_in_64():
     assert starts[-1] + 64 == cw.n_instances  # the last instances: task rows past 2^30
 
 
-@pytest.mark.parametrize("name,every,run", [("C2", 1, 100_000), ("C3", 16, 64), ("C4", 4, 1)])
+@pytest.mark.parametrize("name,every,run", [("C2", 1, 100_000), ("C3", 16, 64), ("C4", 1, 10_000)])
 def test_full_config_sampled(name, every, run):
     cw = gen.CONFIGS[name]
     inputs = _device_batch(cw)
