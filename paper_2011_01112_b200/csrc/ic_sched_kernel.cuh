@@ -628,7 +628,6 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
     return ST_BAD + 200;
   }
   if (rw) {
-    int kmax = 0;
     for (int pos = lane; pos < n; pos += 32) {
       int4* f = S.info + s * p.max_tasks + pos;
       f->x = S.sQ[pos];
@@ -655,20 +654,6 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
         }
       }
       f->y = (f->y & ~255) | ke;
-      kmax = max(kmax, ke);
-    }
-    // one option count for the whole instance: each row's table is padded to the largest
-    // with copies of its last entry (same value and code: the argmin is unchanged), or with an
-    // entry that can never meet the deadline, so the warps sweep one unrolled body per
-    // instance instead of jumping between a body per row (instruction-cache misses)
-    kmax = __reduce_max_sync(0xffffffffu, kmax);
-    for (int pos = lane; pos < n; pos += 32) {
-      int4* f = S.info + s * p.max_tasks + pos;
-      int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
-      const int ke = f->y & 255;
-      const int2 fill = ke > 0 ? rp[ke - 1] : make_int2(0, (1 << 20) * 16 + 1);
-      for (int j = ke; j < kmax; ++j) rp[j] = fill;
-      f->y = (f->y & ~255) | kmax;
     }
   }
   __syncwarp();
