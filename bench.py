@@ -101,12 +101,7 @@ def algorithmic_evals(inputs, n_tasks, opt_stride, delta_micro=0, eps_micro=100_
         Kg = torch.gather(K.view(nb, N), 1, order)
         qg = torch.gather(q.view(nb, N, -1), 1, order[:, :, None].expand(-1, -1, q.shape[1]))
         kk = torch.arange(q.shape[1], device=C.device)[None, None, :]
-        # the kernel drops a depth whose q a shallower fitting depth already reaches (never the
-        # argmin on the reward axis): those are not evaluated
-        fitg = kk < Kg[:, :, None]
-        earlier = torch.tril(torch.ones(q.shape[1], q.shape[1], dtype=torch.bool, device=C.device), -1)
-        dup = ((qg[:, :, :, None] == qg[:, :, None, :]) & earlier & fitg[:, :, None, :]).any(3)
-        ropt = (torch.clamp(qpre[:, :, None] - qg + 1, min=0) * (fitg & ~dup)).sum(2)
+        ropt = (torch.clamp(qpre[:, :, None] - qg + 1, min=0) * (kk < Kg[:, :, None])).sum(2)
         wr_inst = ((qpre + 1) + ropt).sum(1)
         est_t = (torch.clamp(d + 1, min=0).view(nb, N) * (K.view(nb, N) + 1)).sum(1)
         est_r = ((qpre + 1) * (Kg + 1)).sum(1)

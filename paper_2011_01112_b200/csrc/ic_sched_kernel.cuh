@@ -150,10 +150,10 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   for (int k = 0; k < KK; k += 2) {
     if (!GEN || k < kr) {
       const int4 o = k < 8 ? pre[k >> 1] : ops4[k >> 1];  // the first 8 were loaded before the dispatch
-      C[k] = RW ? o.x & 0xFFFF : o.x;  // reward axis: the shift q (bits 16+ hold the depth)
+      C[k] = o.x;
       key[k] = o.y;
       if (k + 1 < KK) {
-        C[k + 1] = RW ? o.z & 0xFFFF : o.z;
+        C[k + 1] = o.z;
         key[k + 1] = o.w;
       }
     }
@@ -168,7 +168,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 #pragma unroll 1
         for (int k = 0; k < kr; ++k) {
           const int2 o = o2[k];
-          a = __viaddmin_s32(cur[max(t - (o.x & 0xFFFF), -1)], o.y, a);
+          a = __viaddmin_s32(cur[max(t - o.x, -1)], o.y, a);
         }
         a = a <= lim ? a : INFV;
         return DROP ? min(cur[t], a) : a;
@@ -633,27 +633,13 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       f->x = S.sQ[pos];
       f->w = pos + 1 < n ? S.sQ[pos + 1] : INT32_MIN;
       // option table in the reward-axis form, once per row here rather than per row and
-      // thread in the sweep: (C, (q << 4) - (k+1)) -> (q | k << 16, C*16 + j+1).  Options
-      // whose quantised reward an earlier (shorter) option already reaches are dropped: from
-      // the same source column P(i-1, r - q) they always finish later, so they are never the
-      // argmin (Eq. 2) and the plan is unchanged.  At Delta = 0.1 most depths share their q
-      // with a shorter one.  The j+1 of the kept options is the decision code (same order as
-      // k, so ties still resolve to the shallower depth); bits 16+ of .x keep the depth k
-      // (q <= 32767 here: the reward row fits the kernel's columns).
+      // thread in the sweep: (C, (q << 4) - (k+1)) -> (q, C*16 + k+1)
       int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
       const int K = f->y & 255;
-      int ke = 0;
       for (int k = 0; k < K; ++k) {
         const int2 o = rp[k];
-        const int q = (o.y + k + 1) >> 4;
-        bool dup = false;
-        for (int j = 0; j < ke; ++j) dup |= (rp[j].x & 0xFFFF) == q;
-        if (!dup) {
-          rp[ke] = make_int2(q | (k << 16), min(o.x, 1 << 20) * 16 + (ke + 1));
-          ++ke;
-        }
+        rp[k] = make_int2((o.y + k + 1) >> 4, min(o.x, 1 << 20) * 16 + (k + 1));
       }
-      f->y = (f->y & ~255) | ke;
     }
   }
   __syncwarp();
@@ -730,8 +716,8 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
     // column the decision of code c at row `pos` (column t) leads to in row pos-1
     auto step = [&](int pos, int tt, int code) -> int {
       if (code == 0) return tt;
-      const int sh = rp[(size_t)pos * p.kp + code - 1].x;  // time axis: C; reward axis: q | depth << 16
-      return rw ? tt - (sh & 0xFFFF) : min(tt, inf[pos].x) - sh;
+      const int sh = rp[(size_t)pos * p.kp + code - 1].x;  // time axis: C; reward axis: q
+      return rw ? tt - sh : min(tt, inf[pos].x) - sh;
     };
     auto nibble = [&](int row, int tt) -> int {
       if (!rw && tt > inf[row].x) {  // past the deadline
@@ -823,7 +809,7 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
   for (int base = 0; base < n; base += 32) {
     const int pos = base + lane;
     const bool valid = pos < n;
-    int code = 0, tk = 0, Cc = 0, r = 0, Sn = 0, depth = -1;
+    int code = 0, tk = 0, Cc = 0, r = 0, Sn = 0;
     if (valid) {
       const int4 f = inf[pos];
       r = f.z;
@@ -835,17 +821,16 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
     if (code > 0) {
       const int2 o = rowp_slot<NW>(p, S, s)[(size_t)pos * p.kp + code - 1];
       Cc = rw ? (o.y - code) >> 4 : o.x;
-      depth = rw ? o.x >> 16 : code - 1;  // reward axis: codes index the pruned table
       a = Cc;
       bb = (long long)r + Cc;
-      Q += rw ? (o.x & 0xFFFF) : (o.y + code) >> 4;
-      {  // R_i(depth), re-read from the (L2-resident) descriptors
+      Q += rw ? o.x : (o.y + code) >> 4;
+      {  // R_i(code-1), re-read from the (L2-resident) descriptors
         const int64_t t = lo + tk;
         long long R = p.mand_conf[t];
-        for (int j = 0; j < depth; ++j) R += p.opt_gain[t * p.smax + j];
+        for (int j = 0; j < code - 1; ++j) R += p.opt_gain[t * p.smax + j];
         conf += R;
       }
-      nopt += depth;
+      nopt += code - 1;
     } else if (valid) {
       ndrop += 1;
     }
@@ -862,7 +847,7 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
     const long long f = max(F + a, bb);
     if (valid) {
       if (code > 0) {
-        p.kept[lo + tk] = (int8_t)depth;
+        p.kept[lo + tk] = (int8_t)(code - 1);
         p.start[lo + tk] = (int32_t)(f - Cc);
         p.finish[lo + tk] = (int32_t)f;
       } else {
