@@ -301,20 +301,38 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       const int g0 = c * CH;
       const int tb = g0 * NT + tid;
       int v[CH];
+      if (g0 + CH <= ng) {
+        // a full chunk (every chunk but this warp's top one): no per-cell predicates, so the
+        // loads of all CH cells share one address per option (immediate offsets u * NT)
 #pragma unroll
-      for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT) : 0;
-      bar_sync(BAR_DP, NT);
+        for (int u = 0; u < CH; ++u) v[u] = cell(tb + u * NT);
+        bar_sync(BAR_DP, NT);
 #pragma unroll
-      for (int w8 = 0; w8 < CH; w8 += 8) {
-        uint32_t dw = 0;
+        for (int w8 = 0; w8 < CH; w8 += 8) {
+          uint32_t dw = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (g0 + w8 + u < ng) {
+          for (int u = 0; u < 8; ++u) {
             dw |= (uint32_t)(v[w8 + u] & 15) << (4 * u);
             nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
           }
+          decrow[((g0 + w8) >> 3) * NT + tid] = dw;
         }
-        if (g0 + w8 < ng) decrow[((g0 + w8) >> 3) * NT + tid] = dw;
+      } else {
+#pragma unroll
+        for (int u = 0; u < CH; ++u) v[u] = (g0 + u < ng) ? cell(tb + u * NT) : 0;
+        bar_sync(BAR_DP, NT);
+#pragma unroll
+        for (int w8 = 0; w8 < CH; w8 += 8) {
+          uint32_t dw = 0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (g0 + w8 + u < ng) {
+              dw |= (uint32_t)(v[w8 + u] & 15) << (4 * u);
+              nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
+            }
+          }
+          if (g0 + w8 < ng) decrow[((g0 + w8) >> 3) * NT + tid] = dw;
+        }
       }
     }
   }
