@@ -22,5 +22,5 @@ from .abi import (  # noqa: F401
     SchedConfig, SchedInfo, SchedTuning, TUNING_FIELDS, Scheduler, use_library, ICSchedError, lib_path, load_library,
     alloc_inputs, alloc_outputs, gen_batch_device,
     IC_SIM_PLANNER, IC_SIM_EDF, IC_SIM_LCF, IC_SIM_RR, IC_SIM_UTIL_EXP, IC_SIM_UTIL_ORACLE,
-    SimConfig, SimResult, simulate, probe_smem,
+    SimConfig, SimResult, simulate, probe_smem, to_micro, confidences_to_inputs,
 )

@@ -484,3 +484,40 @@ def gen_batch_device(seed, n_tasks, n_opt, opt_stride, horizon, u_lo_q16, u_hi_q
     if rc != 0:
         raise ICSchedError("ic_gen_batch_device", rc)
     return t
+
+
+def to_micro(x, dtype=None):
+    """Float confidences (or gains) in [0, 1] -> integer micro-units, round half to even
+    (SURVEY.md §8(b) "Wrapper": ``torch.round(x * 1e6)``; D5 / G11: q = R_µ div Δ_µ needs the
+    decimal value, which binary floating point only reaches after rounding to micro-units).
+
+    ``x``: a torch tensor or anything ``torch.as_tensor`` takes; computed in float64.
+    Returns ``dtype`` (default int32, the ``opt_gain`` layout; use torch.uint32 for
+    ``mand_conf``) on x's device.  Raises ValueError on NaN/inf or values that overflow dtype."""
+    import torch
+    t = torch.as_tensor(x)
+    t = t.to(torch.float64)
+    if not bool(torch.isfinite(t).all()):
+        raise ValueError("to_micro: non-finite confidence")
+    m = torch.round(t * 1e6)  # torch.round rounds half to even
+    dt = torch.int32 if dtype is None else dtype
+    lo, hi = (0, 2**32 - 1) if dt == torch.uint32 else (-2**31, 2**31 - 1)
+    if m.numel() and (float(m.min()) < lo or float(m.max()) > hi):
+        raise ValueError(f"to_micro: value outside the {dt} range")
+    return m.to(torch.int64).to(dt)
+
+
+def confidences_to_inputs(mand_conf, stage_conf):
+    """Float confidence curves -> the ABI's micro-unit fields.
+
+    ``mand_conf`` [T]: confidence after the mandatory stage; ``stage_conf`` [T, S]: confidence
+    after each optional stage (cumulative, P:L48 R_i^L).  Returns (mand_conf uint32 [T],
+    opt_gain int32 [T, S]) where opt_gain[:, l] = micro(conf after stage l) - micro(conf
+    before it), so the prefix sums R_i(k) reproduce the rounded cumulative curve exactly."""
+    import torch
+    m = to_micro(mand_conf, torch.int64)
+    c = to_micro(stage_conf, torch.int64)
+    if c.dim() != 2 or m.dim() != 1 or c.shape[0] != m.shape[0]:
+        raise ValueError("confidences_to_inputs: expected mand_conf [T] and stage_conf [T, S]")
+    prev = torch.cat([m[:, None], c[:, :-1]], dim=1)
+    return m.to(torch.uint32), (c - prev).to(torch.int32)

@@ -65,3 +65,24 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 for pat in ("import oracle", "from oracle", "liboracle", "ic_oracle"):
                     assert pat not in src, (f, pat)
+
+
+def test_to_micro_quantises_like_the_spec():
+    """The wrapper's float -> micro-unit conversion (SURVEY §8(b) "Wrapper", D5/G11): the
+    decimal examples of S:L180-182 and S:L190 quantise as the spec says once the confidences
+    are micro-units (fp64 floor(0.7/0.1) would give 6), and ties round half to even."""
+    import torch
+    from paper_2011_01112_b200 import to_micro, confidences_to_inputs
+    delta = 100_000  # Delta = 0.1 (P:L261)
+    q = to_micro([0.57, 1.0, 0.09, 0.7, 0.3, 0.6], torch.int64) // delta
+    assert q.tolist() == [5, 10, 0, 7, 3, 6]
+    assert to_micro([0.5e-6, 1.5e-6, 2.5e-6, 3.5e-6]).tolist() == [0, 2, 2, 4]
+    m, g = confidences_to_inputs(torch.tensor([0.3, 0.5], dtype=torch.float64),
+                                 torch.tensor([[0.4, 0.7], [0.55, 0.6]], dtype=torch.float64))
+    assert m.dtype == torch.uint32 and g.dtype == torch.int32
+    assert m.to(torch.int64).tolist() == [300000, 500000]
+    assert g.tolist() == [[100000, 300000], [50000, 50000]]
+    with pytest.raises(ValueError):
+        to_micro([float("nan")])
+    with pytest.raises(ValueError):
+        to_micro([-0.1], torch.uint32)

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 run() {  # $1 = label, $2 = config[:instances], $3 = library ("" = in-tree)
   local c=${2%%:*} n=${2#*:}; [ "$n" = "$2" ] && n=0
-  IC_SCHED_LIB=$3 timeout 600 python bench.py --config $c --instances $n --no-cpu-baseline --no-e2e $EXTRA 2>/dev/null | tail -1 |
+  timeout 600 python bench.py ${3:+--lib $3} --config $c --instances $n --no-cpu-baseline --no-e2e $EXTRA 2>/dev/null | tail -1 |
     python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1 $2', round(d['value']), round(d['roofline']['frac'],4), round(d['ms_per_step'],3), d.get('result_hash'))"
 }
 for rep in 1 2; do
