@@ -124,7 +124,8 @@ int ic_sched_create(const ic_sched_config* cfg, ic_sched** out);
  * process environment.  Results are identical for every valid tuning;
  * IC_ERR_INVALID_ARG for out-of-range fields. */
 typedef struct {
-  int32_t dp_warps;      /* 1, 2, 4, 8 or 16 DP warps per instance (default: ~32 column groups per thread) */
+  int32_t dp_warps;      /* 1, 2, 4, 8, 15 or 16 DP warps per instance (default: ~32 column groups per thread;
+                            15: with the tail warp 4 warps per SM sub-partition, 128 registers) */
   int32_t pad_cols;      /* NEG pad left of column 0 in ticks (default: grown into spare shared memory)      */
   int32_t in_place;      /* 1: rows updated in place (forces >= 8 DP warps); default only when H needs it     */
   int32_t slots;         /* 1: setup and sweep serialised (one table slot); default 2 when they fit           */

@@ -26,6 +26,7 @@ KernelFn kernel_for(int nw, bool sb, bool drop) {
     case 2: return icsched::kernel_nw2(sb, drop);
     case 4: return icsched::kernel_nw4(sb, drop);
     case 8: return icsched::kernel_nw8(sb, drop);
+    case 15: return icsched::kernel_nw15(sb, drop);
     case 16: return icsched::kernel_nw16(sb, drop);
     default: return nullptr;
   }
@@ -106,13 +107,28 @@ Layout make_solo_layout(const ic_sched_config& c, int pad, int cap_cols = 0) {
   L.off_task = o;   o = align16(o + mt * 4);
   L.off_tail = o;
   L.off_misc = o;   o = align16(o + 24 * 8);  // [0..15] instance header, [16..23] stats
-  L.off_chosen = o; o = align16(o + mt * 4);
-  L.off_sd = o;     o = align16(o + mt * 4);
-  L.off_sr = o;     o = align16(o + mt * 4);
-  L.off_sS = o;     o = align16(o + mt * 4);
-  L.off_key = o;    o = align16(o + L.np2 * 8);
   L.off_aux = o;    o = align16(o + mt * 4);
-  L.off_sQ = o;     o = align16(o + mt * 4);
+  // The setup's staging (sd, sr, sS, sQ, sort keys) and the backtrack's chosen codes are
+  // never live during the sweep, and the sweep initialises every column it reads: they
+  // share the row's column area (never the pad, whose contents persist across instances).
+  // Fewer bytes per warp, more resident warps (C3 at Delta = 0.1: 17 -> 20 warps per SM).
+  const int staged = align16(mt * 4) * 5 + align16(L.np2 * 8);
+  int so = L.off_rowbuf + ((pad * 4 + 15) & ~15);  // the first column (past the pad)
+  if (so + staged <= L.off_rowbuf + L.rs * 4) {
+    L.off_chosen = so; so += align16(mt * 4);
+    L.off_sd = so;     so += align16(mt * 4);
+    L.off_sr = so;     so += align16(mt * 4);
+    L.off_sS = so;     so += align16(mt * 4);
+    L.off_sQ = so;     so += align16(mt * 4);
+    L.off_key = so;
+  } else {
+    L.off_chosen = o; o = align16(o + mt * 4);
+    L.off_sd = o;     o = align16(o + mt * 4);
+    L.off_sr = o;     o = align16(o + mt * 4);
+    L.off_sS = o;     o = align16(o + mt * 4);
+    L.off_key = o;    o = align16(o + L.np2 * 8);
+    L.off_sQ = o;     o = align16(o + mt * 4);
+  }
   L.cap = cap;
   L.bytes = o;  // per warp
   return L;
@@ -185,7 +201,7 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   int nw = 1;
   while (nw < 16 && 32 * nw * 32 < c.max_horizon) nw *= 2;
   if (tu.dp_warps) nw = tu.dp_warps;
-  if (nw != 1 && nw != 2 && nw != 4 && nw != 8 && nw != 16) return IC_ERR_INVALID_ARG;
+  if (nw != 1 && nw != 2 && nw != 4 && nw != 8 && nw != 15 && nw != 16) return IC_ERR_INVALID_ARG;
   // NEG pad left of column 0: rows whose longest usable option reaches further use
   // the masked general path, so the pad only trades shared memory for speed.
   int pad = c.max_horizon / 16 < 64 ? 64 : (c.max_horizon / 16 > 256 ? 256 : c.max_horizon / 16);

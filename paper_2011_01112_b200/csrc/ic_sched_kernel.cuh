@@ -122,6 +122,13 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
+// the least column t >= first that thread tid owns (t = tid mod NT; NT need not be a power of 2)
+template <int NT>
+__device__ __forceinline__ int first_col(int first, int tid) {
+  if constexpr ((NT & (NT - 1)) == 0) return first + ((tid - first) & (NT - 1));
+  int m = (tid - first) % NT;
+  return first + (m < 0 ? m + NT : m);
+}
 
 // ---------------------------------------------------------------------------
 // DP warps: one row, active columns t <= d.  K options (compile-time), or GEN = the
@@ -1063,7 +1070,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       M = srow[p.H];
       for (int t = tid; t <= dprev; t += NT) dst[t] = srow[t];
       const int first = dprev + 1 > 0 ? dprev + 1 : 0;
-      for (int t = first + ((tid - first) & (NT - 1)); t <= dk; t += NT) dst[t] = rw ? INFV : M;
+      for (int t = first_col<NT>(first, tid); t <= dk; t += NT) dst[t] = rw ? INFV : M;
       bar_sync(BAR_DP, NT);
     }
     int4 f = inf[k0];
@@ -1107,7 +1114,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         if (dn > d) {
           const int first = d + 1 > 0 ? d + 1 : 0;
 #pragma unroll 1
-          for (int t = first + ((tid - first) & (NT - 1)); t <= dn; t += NT) nxt[t] = Mn;
+          for (int t = first_col<NT>(first, tid); t <= dn; t += NT) nxt[t] = Mn;
         }
         M = Mn;
         if (keep_state) {  // keep checkpoint rows for later re-plans: active columns, tail value
@@ -1177,6 +1184,7 @@ KernelFn kernel_nw1(bool sb, bool drop);
 KernelFn kernel_nw2(bool sb, bool drop);
 KernelFn kernel_nw4(bool sb, bool drop);
 KernelFn kernel_nw8(bool sb, bool drop);
+KernelFn kernel_nw15(bool sb, bool drop);
 KernelFn kernel_nw16(bool sb, bool drop);
 
 }  // namespace icsched

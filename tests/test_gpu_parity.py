@@ -185,6 +185,7 @@ def test_decision_placement(decisions):
                                     dict(pad_cols=32), dict(slots=1, dp_warps=2),
                                     dict(slots=1, in_place=1, dp_warps=8), dict(option_tables=1, dp_warps=8),
                                     dict(option_tables=1, in_place=1, dp_warps=16),
+                                    dict(in_place=1, dp_warps=15), dict(dp_warps=15), dict(option_tables=1, in_place=1, dp_warps=15),
                                     dict(option_tables=1, dp_warps=8, decisions=2), dict(no_vec_loads=1),
                                     dict(decisions=1, dp_warps=2)])
 @pytest.mark.parametrize("mode", [0, 1])
