@@ -136,6 +136,8 @@ typedef struct {
   int32_t ctas_per_sm;   /* cap on resident CTAs per SM (default: occupancy)                                 */
   int32_t no_vec_loads;  /* 1: scalar descriptor loads only                                                  */
   int32_t kernel;        /* 1: warp-specialised kernel; 2: one warp per instance; default by shape          */
+  int32_t packed_options;/* 2: int2 option tables in the one-warp kernel; default packed 32-bit entries when
+                            a fixed Delta >= 489 micro and H <= 4096 bound every field to 16 bits      */
 } ic_sched_tuning;
 int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_tuning* tuning, ic_sched** out);
 
@@ -223,6 +225,7 @@ typedef struct {
   int32_t smem_bytes, decisions_in_smem, double_buffered, pad_cols;
   int64_t workspace_bytes;
   int32_t kernels_per_solve, hybrid;
+  int32_t packed_options;  /* 1: the one-warp kernel holds packed option entries */
 } ic_sched_info;
 int ic_sched_get_info(const ic_sched* h, ic_sched_info* info);
 

@@ -52,7 +52,7 @@ class SchedConfig(ctypes.Structure):
 
 
 TUNING_FIELDS = ("dp_warps", "pad_cols", "in_place", "slots", "decisions", "option_tables", "axis", "ckpt",
-                 "ctas_per_sm", "no_vec_loads", "kernel")
+                 "ctas_per_sm", "no_vec_loads", "kernel", "packed_options")
 
 
 class SchedTuning(ctypes.Structure):
@@ -70,7 +70,7 @@ class SchedInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("threads_per_cta", "cols_per_thread", "ctas_per_sm", "grid",
                                               "smem_bytes", "decisions_in_smem", "double_buffered",
                                               "pad_cols")] + [("workspace_bytes", ctypes.c_int64)] + \
-        [(n, ctypes.c_int32) for n in ("kernels_per_solve", "hybrid")]
+        [(n, ctypes.c_int32) for n in ("kernels_per_solve", "hybrid", "packed_options")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

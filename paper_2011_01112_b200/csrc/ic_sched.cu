@@ -83,13 +83,15 @@ Layout make_layout(const ic_sched_config& c, int nw, bool sb, int pad, bool dec_
 
 // One warp's private region in the solo kernel (ic_solo_kernel.cuh): a single in-place row
 // and one slot of the per-task tables.  Offsets are relative to the warp's base.
-Layout make_solo_layout(const ic_sched_config& c, int pad, int cap_cols = 0) {
+Layout make_solo_layout(const ic_sched_config& c, int pad, int cap_cols = 0, bool packed = false) {
   Layout L{};
   const int cols = ((cap_cols ? cap_cols : c.max_horizon) + 31) / 32;
   const int cap = 32 * cols;
   const int mt = c.max_tasks;
   L.nq = (cols + 7) / 8;
-  L.kp = (c.max_opt_stages + 2) & ~1;
+  // option entries per row: int2 pairs (even count, 16-byte rows), or packed words (a
+  // multiple of 4); the table ends with 64 bytes of slack for the sweep's 4 x int4 preload
+  L.kp = packed ? (c.max_opt_stages + 4) & ~3 : (c.max_opt_stages + 2) & ~1;
   L.r1 = c.max_opt_stages + 1;
   int np2 = 1;
   while (np2 < mt) np2 <<= 1;
@@ -102,7 +104,7 @@ Layout make_solo_layout(const ic_sched_config& c, int pad, int cap_cols = 0) {
   int o = 0;
   L.off_rowbuf = o; o = align16(o + L.rs * 4);
   L.off_dec = o;
-  L.off_rowp = o;   o = align16(o + (mt * L.kp + 8) * 8);
+  L.off_rowp = o;   o = align16(o + mt * L.kp * (packed ? 4 : 8) + 64);
   L.off_info = o;   o = align16(o + mt * 16);
   L.off_task = o;   o = align16(o + mt * 4);
   L.off_tail = o;
@@ -169,6 +171,7 @@ struct ic_sched {
   int axis_mode;       // tuning, fixed at create: 0 auto per instance, 1 time, 2 reward
   int ckpt;            // re-plan checkpoint spacing (rows), power of two
   int no_vec_loads;    // 1: scalar descriptor loads only
+  int solo_packed;     // the solo kernel's option tables hold packed words
 };
 
 extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
@@ -189,7 +192,7 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   if (tu.dp_warps < 0 || tu.pad_cols < 0 || tu.in_place < 0 || tu.in_place > 1 || tu.slots < 0 || tu.slots > 2 ||
       tu.decisions < 0 || tu.decisions > 2 || tu.option_tables < 0 || tu.option_tables > 1 || tu.axis < 0 ||
       tu.axis > 2 || tu.ckpt < 0 || (tu.ckpt & (tu.ckpt - 1)) != 0 || tu.ctas_per_sm < 0 || tu.no_vec_loads < 0 ||
-      tu.no_vec_loads > 1 || tu.kernel < 0 || tu.kernel > 2)
+      tu.no_vec_loads > 1 || tu.kernel < 0 || tu.kernel > 2 || tu.packed_options < 0 || tu.packed_options > 2)
     return IC_ERR_INVALID_ARG;
   if (cudaSetDevice(c.device) != cudaSuccess) return IC_ERR_CUDA;
   int sms = 0;
@@ -200,6 +203,9 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   // DP warps per instance: about 32 column groups per thread (tuning.dp_warps overrides).
   int nw = 1;
   while (nw < 16 && 32 * nw * 32 < c.max_horizon) nw *= 2;
+  // 16 DP warps + the tail warp = 17 warps: 5 on one SM sub-partition caps the registers at 96
+  // (spills); 15 + 1 = 4 per sub-partition, 128 registers (C4: 6.07e4 -> 6.82e4 instances/s)
+  if (nw == 16) nw = 15;
   if (tu.dp_warps) nw = tu.dp_warps;
   if (nw != 1 && nw != 2 && nw != 4 && nw != 8 && nw != 15 && nw != 16) return IC_ERR_INVALID_ARG;
   // NEG pad left of column 0: rows whose longest usable option reaches further use
@@ -315,10 +321,15 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   if (solo || hybrid) {
     int rc = IC_OK;
     const int spad = tu.pad_cols ? ((tu.pad_cols + 31) & ~31) : 64 > c.max_horizon ? ((c.max_horizon + 31) & ~31) : 64;
-    Layout S = make_solo_layout(c, spad, hybrid ? (int)qcap : 0);
+    // packed option entries (one word per option: more resident warps) whenever a fixed Delta
+    // bounds q <= 1e6 / Delta <= 2047 and the horizon bounds C <= 4095 (ic_sched_kernel.cuh pk_get)
+    const bool packed = tu.packed_options != 2 && c.delta_micro > 0 && 1000000 / c.delta_micro <= 2047 &&
+                        c.max_horizon <= 4096;
+    Layout S = make_solo_layout(c, spad, hybrid ? (int)qcap : 0, packed);
     h->hybrid = hybrid ? 1 : 0;
-    KernelFn sf = icsched::kernel_solo(drop, false);
-    KernelFn sfs = icsched::kernel_solo(drop, true);
+    h->solo_packed = packed ? 1 : 0;
+    KernelFn sf = icsched::kernel_solo(drop, false, packed);
+    KernelFn sfs = icsched::kernel_solo(drop, true, packed);
     const int bytes = S.bytes * IC_SOLO_WPC;
     int sp = 0;
     if (bytes > kSmemLimit) rc = IC_ERR_LIMIT;
@@ -384,6 +395,7 @@ extern "C" int ic_sched_get_info(const ic_sched* h, ic_sched_info* info) {
     info->workspace_bytes = h->solo_dec_warp_words * 4 * h->solo_grid * IC_SOLO_WPC;
     info->kernels_per_solve = h->hybrid ? 2 : 1;
     info->hybrid = h->hybrid;
+    info->packed_options = h->solo_packed;
     return IC_OK;
   }
   info->kernels_per_solve = 1;
@@ -563,6 +575,7 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
     p.pad = S.pad;
     p.nq = S.nq;
     p.np2 = S.np2;
+    p.kp = S.kp;
     p.dec_smem = 0;
     p.dec_global = h->solo_dec;
     p.dec_slab_words = h->solo_dec_warp_words;

@@ -122,12 +122,54 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ int viaddmax(int a, int b, int c) { return __viaddmax_s32(a, b, c); }
+// Shared-memory load at a 32-bit shared address.  The double-buffered sweep addresses its row
+// through one opaque shared base per row (cvta below) so the window base is not re-derived
+// (S2UR) at the head of every chunk's address chain; ptxas folds the constant cell offsets
+// into the LDS immediates.  Volatile: never merged across the row barriers.
+__device__ __forceinline__ int lds32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, int v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  uint32_t a;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+  return a;
+}
 // the least column t >= first that thread tid owns (t = tid mod NT; NT need not be a power of 2)
 template <int NT>
 __device__ __forceinline__ int first_col(int first, int tid) {
   if constexpr ((NT & (NT - 1)) == 0) return first + ((tid - first) & (NT - 1));
   int m = (tid - first) % NT;
   return first + (m < 0 ? m + NT : m);
+}
+
+// Packed option entries (the solo kernel at a fixed Delta, PK): one 32-bit word per option
+// instead of an int2, two 16-bit fields.  Time axis: shift C (low, unsigned) and key
+// (q << 4) - (k+1) (high, signed); reward axis: addend C*16 + k+1 (low, unsigned) and shift q
+// (high).  The host enables it only when every field fits (q <= 2047, C <= 4095).
+// The int2 form is (shift, addend) on both axes.
+__device__ __forceinline__ int2 pk_get(int e, bool rw) {
+  const int lo = e & 0xFFFF, hi = e >> 16;
+  return rw ? make_int2(hi, lo) : make_int2(lo, hi);
+}
+__device__ __forceinline__ int pk_put(int2 v, bool rw) {
+  return rw ? (int)((unsigned)(v.y & 0xFFFF) | ((unsigned)v.x << 16)) : (int)((unsigned)(v.x & 0xFFFF) | ((unsigned)v.y << 16));
+}
+template <bool PK>
+__device__ __forceinline__ int2 opt_get(const int2* tab, size_t idx, bool rw) {
+  if constexpr (PK) return pk_get(((const int*)tab)[idx], rw);
+  return tab[idx];
+}
+template <bool PK>
+__device__ __forceinline__ void opt_put(int2* tab, size_t idx, int2 v, bool rw) {
+  if constexpr (PK)
+    ((int*)tab)[idx] = pk_put(v, rw);
+  else
+    tab[idx] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -140,7 +182,7 @@ __device__ __forceinline__ int first_col(int first, int tid) {
 // reward r; option k shifts by q_k and adds C_k*16 + (k+1) (the code), so one
 // VIADDMNMX (add + min) per option yields value and argmin, ties to the smaller
 // code (drop, then fewer stages).  Admits are valid iff P <= d_i ("lim").
-template <int NW, bool SB, bool DROP, int K, bool GEN, bool RW>
+template <int NW, bool SB, bool DROP, int K, bool GEN, bool RW, bool PK = false>
 __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
                                        const int4* __restrict__ ops4, const int4 (&pre)[4], const int d,
                                        const int r, const int kr, const int lim) {
@@ -151,17 +193,33 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   constexpr int KK = RTK ? 0 : GEN ? KMAX : K;
   // one-warp rows are swept by warp 0 of the warp-specialised kernel or by any warp of the
   // solo kernel: the lane is the thread's column offset there
-  const int tid = NW == 1 ? (int)(threadIdx.x & 31) : (int)threadIdx.x, warp = NW == 1 ? 0 : tid >> 5;
+  // the thread index through an opaque read: kept in a register for the whole row instead of
+  // re-read (S2R) at the head of every chunk's address chain under register pressure
+  int tix;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tix));
+  const int tid = NW == 1 ? (tix & 31) : tix, warp = NW == 1 ? 0 : tid >> 5;
   int C[KK > 0 ? KK : 1], key[KK > 0 ? KK : 1];
+  if constexpr (PK) {  // 16 packed entries were loaded before the dispatch
 #pragma unroll
-  for (int k = 0; k < KK; k += 2) {
-    if (!GEN || k < kr) {
-      const int4 o = k < 8 ? pre[k >> 1] : ops4[k >> 1];  // the first 8 were loaded before the dispatch
-      C[k] = o.x;
-      key[k] = o.y;
-      if (k + 1 < KK) {
-        C[k + 1] = o.z;
-        key[k + 1] = o.w;
+    for (int k = 0; k < KK; ++k) {
+      if (!GEN || k < kr) {
+        const int4 o = pre[k >> 2];
+        const int2 e = pk_get((k & 3) == 0 ? o.x : (k & 3) == 1 ? o.y : (k & 3) == 2 ? o.z : o.w, RW);
+        C[k] = e.x;
+        key[k] = e.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < KK; k += 2) {
+      if (!GEN || k < kr) {
+        const int4 o = k < 8 ? pre[k >> 1] : ops4[k >> 1];  // the first 8 were loaded before the dispatch
+        C[k] = o.x;
+        key[k] = o.y;
+        if (k + 1 < KK) {
+          C[k + 1] = o.z;
+          key[k + 1] = o.w;
+        }
       }
     }
   }
@@ -174,7 +232,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         int a = INFV;
 #pragma unroll 1
         for (int k = 0; k < kr; ++k) {
-          const int2 o = o2[k];
+          const int2 o = opt_get<PK>(o2, k, RW);
           a = __viaddmin_s32(cur[max(t - o.x, -1)], o.y, a);
         }
         a = a <= lim ? a : INFV;
@@ -183,7 +241,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         int v = DROP ? cur[t] : NEG;
 #pragma unroll 1
         for (int k = 0; k < kr; ++k) {
-          const int2 o = o2[k];
+          const int2 o = opt_get<PK>(o2, k, RW);
           const int src = t - o.x;
           v = viaddmax(cur[src >= r ? src : -1], o.y, v);
         }
@@ -217,6 +275,35 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
   auto stv = [](int v) { return RW ? (v & ~15) : (v | 15); };
   if constexpr (!SB) {
     constexpr int BATCH = (KK <= IC_BATCH_KSPLIT) ? 8 : IC_BATCH_HI;  // cells whose loads are in flight together
+    // full chunks of the common rows (no bounds): loads through the row's opaque shared base
+    const uint32_t cs = smem_addr(cur), ns = smem_addr(nxt);
+    auto cell_s = [&](int t) -> int {
+      const uint32_t at = cs + 4u * (uint32_t)t;
+      if constexpr (RW) {
+        int a = INFV;
+#pragma unroll
+        for (int k = 0; k < KK; ++k) a = __viaddmin_s32(lds32(at - 4u * (uint32_t)C[k]), key[k], a);
+        a = a <= lim ? a : INFV;
+        return DROP ? min(lds32(at), a) : a;
+      } else {
+        int v = DROP ? lds32(at) : NEG;
+#pragma unroll
+        for (int k = 0; k < KK; ++k) v = viaddmax(lds32(at - 4u * (uint32_t)C[k]), key[k], v);
+        return v;
+      }
+    };
+    auto cellx = [&](int t) -> int {
+      if constexpr (GEN)
+        return cell(t);
+      else
+        return cell_s(t);
+    };
+    auto store = [&](int t, int v) {
+      if constexpr (GEN)
+        nxt[t] = stv(v);
+      else
+        sts32(ns + 4u * (uint32_t)t, stv(v));
+    };
     for (int g0 = 0; g0 < ng; g0 += 8) {
       const int tb = g0 * NT + tid;
       uint32_t dw = 0;
@@ -225,11 +312,11 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         for (int h = 0; h < 8; h += BATCH) {
           int v[BATCH];
 #pragma unroll
-          for (int u = 0; u < BATCH; ++u) v[u] = cell(tb + (h + u) * NT);
+          for (int u = 0; u < BATCH; ++u) v[u] = cellx(tb + (h + u) * NT);
 #pragma unroll
           for (int u = 0; u < BATCH; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (h + u));
-            nxt[tb + (h + u) * NT] = stv(v[u]);
+            store(tb + (h + u) * NT, v[u]);
           }
         }
       } else {
@@ -240,11 +327,11 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
           constexpr int NB = decltype(nb_tag)::value;
           int v[NB];
 #pragma unroll
-          for (int u = 0; u < NB; ++u) v[u] = cell(tb + (u0 + u) * NT);
+          for (int u = 0; u < NB; ++u) v[u] = cellx(tb + (u0 + u) * NT);
 #pragma unroll
           for (int u = 0; u < NB; ++u) {
             dw |= (uint32_t)(v[u] & 15) << (4 * (u0 + u));
-            nxt[tb + (u0 + u) * NT] = stv(v[u]);
+            store(tb + (u0 + u) * NT, v[u]);
           }
           u0 += NB;
         };
@@ -348,16 +435,16 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 // gen: the row takes the general path (releases, or an option longer than the pad).
 // KC: the largest option count with its own unrolled sweep; rows with more take the
 // general path (the solo kernel compiles K <= 9, i.e. up to 8 optional stages).
-template <int NW, bool SB, bool DROP, bool RW, int KC = 15>
+template <int NW, bool SB, bool DROP, bool RW, int KC = 15, bool PK = false>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
                                                 uint32_t* decrow, const int4* ops4, int d, int r, int lim) {
   const int4 pre[4] = {ops4[0], ops4[1], ops4[2], ops4[3]};  // issued ahead of the K dispatch
   if (gen || K > KC) {
-    dp_row<NW, SB, DROP, KMAX, true, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim);
+    dp_row<NW, SB, DROP, KMAX, true, RW, PK>(cur, nxt, decrow, ops4, pre, d, r, K, lim);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: if constexpr (KK <= KC) dp_row<NW, SB, DROP, KK, false, RW>(cur, nxt, decrow, ops4, pre, d, r, K, lim); break;
+  case KK: if constexpr (KK <= KC) dp_row<NW, SB, DROP, KK, false, RW, PK>(cur, nxt, decrow, ops4, pre, d, r, K, lim); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -522,7 +609,7 @@ __device__ __forceinline__ void for_each_opt(const Params& p, int64_t t, int Sn,
 // Pass 1 (input order): validation, the best individually feasible reward
 // (Theorem 1's R), the EDF keys.  Pass 2 (EDF order, descriptors re-read):
 // prefix sums, q = R div Delta, packed keys, the row table of the DP.
-template <int NW>
+template <int NW, bool PK = false>
 __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int lane,
                           unsigned long long* acc) {
   const int64_t lo = p.task_begin[b];
@@ -590,13 +677,16 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       const int64_t t = lo + tk;
       d = S.sd[tk];
       const int r = S.sr[tk], Sn = S.sS[tk];
-      int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
+      int2* rp = rowp_slot<NW>(p, S, s);
+      const size_t r0 = (size_t)pos * p.kp;
       long long C = p.mand_wcet[t], R = p.mand_conf[t];
+      int Clast = 0;
       auto option = [&](int k) {
         if (C <= (long long)d - r) {  // options that can fit (C increasing in k); only they
           const int q = (int)(R / delta);  // bound the packed keys and the reward columns
           qmax = max(qmax, q);
-          rp[k] = make_int2((int)C, (q << 4) - (k + 1));
+          opt_put<PK>(rp, r0 + k, make_int2((int)C, (q << 4) - (k + 1)), false);
+          Clast = (int)C;
           K = k + 1;
         }
       };
@@ -607,7 +697,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
         option(k);
       });
       // the general path: releases, or (per axis) an option reaching past the pad
-      const bool gen = r > 0 || (K > 0 && rp[K - 1].x > p.pad);
+      const bool gen = r > 0 || (K > 0 && Clast > p.pad);
       const bool genr = qmax > p.pad;
       anyrel |= r > 0;
       const int dn = pos + 1 < n ? S.sd[(int)(S.key[pos + 1] & 0xFFF)] : INT32_MIN;
@@ -659,11 +749,12 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       f->w = pos + 1 < n ? S.sQ[pos + 1] : INT32_MIN;
       // option table in the reward-axis form, once per row here rather than per row and
       // thread in the sweep: (C, (q << 4) - (k+1)) -> (q, C*16 + k+1)
-      int2* rp = rowp_slot<NW>(p, S, s) + (size_t)pos * p.kp;
+      int2* rp = rowp_slot<NW>(p, S, s);
+      const size_t r0 = (size_t)pos * p.kp;
       const int K = f->y & 255;
       for (int k = 0; k < K; ++k) {
-        const int2 o = rp[k];
-        rp[k] = make_int2((o.y + k + 1) >> 4, min(o.x, 1 << 20) * 16 + (k + 1));
+        const int2 o = opt_get<PK>(rp, r0 + k, false);
+        opt_put<PK>(rp, r0 + k, make_int2((o.y + k + 1) >> 4, min(o.x, 1 << 20) * 16 + (k + 1)), true);
       }
     }
   }
@@ -722,7 +813,7 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
 // SOLO: the solo kernel keeps no tail nibbles; a column past a row's deadline takes the
 // decision of the deadline column itself (every G_i(t), t > d_i, equals G_i(d_i) with the
 // same argmax: the options read G_{i-1}(d_i - C_k) and the drop reads M_{i-1} there).
-template <int NW, bool SOLO = false>
+template <int NW, bool SOLO = false, bool PK = false>
 __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, int s, int lane, int db) {
   constexpr int NT = 32 * NW;
   const long long* mi = S.misc + s * 16;
@@ -741,7 +832,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
     // column the decision of code c at row `pos` (column t) leads to in row pos-1
     auto step = [&](int pos, int tt, int code) -> int {
       if (code == 0) return tt;
-      const int sh = rp[(size_t)pos * p.kp + code - 1].x;  // time axis: C; reward axis: q
+      const int sh = opt_get<PK>(rp, (size_t)pos * p.kp + code - 1, rw).x;  // time axis: C; reward axis: q
       return rw ? tt - sh : min(tt, inf[pos].x) - sh;
     };
     auto nibble = [&](int row, int tt) -> int {
@@ -821,7 +912,7 @@ __device__ __forceinline__ void discard_decisions(const Params& p, const Smem& S
 }
 
 // a7/a8: EDF schedule (warp max-plus scan), outputs in input order, stats.
-template <int NW>
+template <int NW, bool PK = false>
 __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int s, int lane,
                                              unsigned long long* acc) {
   const long long* mi = S.misc + s * 16;
@@ -844,7 +935,7 @@ __device__ __forceinline__ void tail_outputs(const Params& p, const Smem& S, int
     }
     long long a = 0, bb = -(1LL << 62);  // map x -> max(x + a, bb)
     if (code > 0) {
-      const int2 o = rowp_slot<NW>(p, S, s)[(size_t)pos * p.kp + code - 1];
+      const int2 o = opt_get<PK>(rowp_slot<NW>(p, S, s), (size_t)pos * p.kp + code - 1, rw);
       Cc = rw ? (o.y - code) >> 4 : o.x;
       a = Cc;
       bb = (long long)r + Cc;

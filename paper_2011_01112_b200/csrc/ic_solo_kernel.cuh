@@ -62,13 +62,14 @@ __device__ __forceinline__ unsigned long long* solo_acc(const Params& p, unsigne
 // a1-a3 for instance b (tail_setup); ST_OK if the sweep must run.  The three phases are
 // separate (non-inlined) functions so that each gets the whole register budget: the
 // setup's sort keys and the sweep's option tables are never live at the same time.
+template <bool PK>
 static __device__ __noinline__ int solo_setup(const Params& p, unsigned char* base, int64_t b, int lane) {
   const Smem S = solo_smem(p, base, nullptr);
-  return tail_setup<1>(p, S, b, 0, lane, solo_acc(p, base));
+  return tail_setup<1, PK>(p, S, b, 0, lane, solo_acc(p, base));
 }
 
 // a4 + a5: the rows in place, then the optimum of row N into misc[5], misc[6].
-template <bool DROP, bool STATE>
+template <bool DROP, bool STATE, bool PK>
 __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
   // (dec: the warp's decision slab; replaced by the instance's state when one is kept)
   int32_t* const rowbuf = (int32_t*)(base + p.off_rowbuf);
@@ -100,7 +101,8 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
   const int32_t* aux = (const int32_t*)(base + p.off_aux);
   const int kp = p.kp;
   const int dec_row_words = p.nq * 32;
-  const int2* ops = (const int2*)(base + p.off_rowp) + k0 * kp;
+  // option entries of row pos start at entry pos * kp (int2, or one packed word with PK)
+  const char* ops = (const char*)(base + p.off_rowp) + (size_t)k0 * kp * (PK ? 4 : 8);
   uint32_t* decrow = dec + (size_t)k0 * dec_row_words;
   int M = 15;
   if (STATE && k0 > 0) {  // restore row k0-1 (its active columns, then its tail value up to d_k0)
@@ -118,14 +120,14 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
     const int d = f.x, K = f.y & 255;
     if (rw) {
       // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
-      dp_row_dispatch<1, true, DROP, true, IC_SOLO_KC>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
+      dp_row_dispatch<1, true, DROP, true, IC_SOLO_KC, PK>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
       __syncwarp();
       if (STATE && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
         int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * (p.H + 1);
         for (int t = lane; t <= d; t += 32) srow[t] = buf[t];
       }
     } else {
-      dp_row_dispatch<1, true, DROP, false, IC_SOLO_KC>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
+      dp_row_dispatch<1, true, DROP, false, IC_SOLO_KC, PK>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
       __syncwarp();
       // M_pos = G_pos(d) (tail collapse); G_pos(t) = M_pos on (d, d_next] for the next row
       if (d >= 0)
@@ -143,7 +145,7 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
       for (int t = first + lane; t <= dn; t += 32) buf[t] = M;
       __syncwarp();
     }
-    ops += kp;
+    ops += kp * (PK ? 4 : 8);
     decrow += dec_row_words;
   }
   // a5: the optimum of row N
@@ -185,16 +187,17 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
 }
 
 // a6-a8: backtrack, schedule times and outputs, stats.
+template <bool PK>
 static __device__ __noinline__ void solo_finish(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
   const Smem S = solo_smem(p, base, dec);
-  tail_backtrack<1, true>(p, S, 0, lane, 0);
+  tail_backtrack<1, true, PK>(p, S, 0, lane, 0);
   discard_decisions<1>(p, S, 0, lane, 0);
-  tail_outputs<1>(p, S, 0, lane, solo_acc(p, base));
+  tail_outputs<1, PK>(p, S, 0, lane, solo_acc(p, base));
 }
 
 // STATE: the re-plan entry points (decisions and checkpoint rows kept in the caller's state);
 // plain solves run the variant without any of that code.
-template <bool DROP, bool STATE>
+template <bool DROP, bool STATE, bool PK>
 __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -210,10 +213,10 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
       unsigned long long v = 0;
       if (lane == 0) v = atomicAdd(&p.work[0], 1ull);
       b = (int64_t)__shfl_sync(0xffffffffu, v, 0);
-    } while (b < p.B && solo_setup(p, base, b, lane) != ST_OK);
+    } while (b < p.B && solo_setup<PK>(p, base, b, lane) != ST_OK);
     if (b >= p.B) break;
-    solo_sweep<DROP, STATE>(p, base, dec, lane);
-    solo_finish(p, base, dec, lane);
+    solo_sweep<DROP, STATE, PK>(p, base, dec, lane);
+    solo_finish<PK>(p, base, dec, lane);
   }
   __syncwarp();
   if (lane < 8 && p.stats && acc[lane]) atomicAdd(&p.stats[lane], acc[lane]);
@@ -226,6 +229,6 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
   }
 }
 
-KernelFn kernel_solo(bool drop, bool state);
+KernelFn kernel_solo(bool drop, bool state, bool packed);
 
 }  // namespace icsched

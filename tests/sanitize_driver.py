@@ -25,6 +25,8 @@ VARIANTS = {
     "nw4": ({}, "C3", 2, 0),
     "sb8_inplace": (dict(in_place=1, dp_warps=8), "C3", 2, 0),
     "nw16_global_tables": (dict(in_place=1, dp_warps=16, option_tables=1), "C3", 2, 0),
+    "nw15_global_tables": (dict(in_place=1, dp_warps=15, option_tables=1), "C3", 2, 0),
+    "solo_unpacked": (dict(packed_options=2), "C2", 6, 100_000),
     "reward_axis": (dict(axis=2, kernel=1), "C2", 6, 100_000),
     "solo": ({}, "C2", 6, 0),
     "solo_reward": ({}, "C2", 6, 100_000),

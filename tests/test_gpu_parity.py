@@ -394,11 +394,13 @@ def test_solo_and_warp_specialised_kernels_agree(name, n, delta, mode):
     ocfg = OracleConfig(drop_mode=mode, delta_micro=delta, epsilon_micro=cw.epsilon_micro, max_tasks=cw.n_tasks,
                         max_horizon=cw.horizon)
     ref = oracle.solve(batch, ocfg, TIME)
-    for kernel in (0, 1, 2):
+    for tuning in (dict(kernel=0), dict(kernel=1), dict(kernel=2), dict(kernel=0, packed_options=2)):
         got = gpu_solve(batch, max_tasks=cw.n_tasks, max_opt=cw.n_opt, max_horizon=cw.horizon, drop_mode=mode,
-                        delta=delta, eps=cw.epsilon_micro, tuning=dict(kernel=kernel))
-        assert_parity(got, ref, f"{name} kernel={kernel} delta={delta} mode={mode}")
-        assert (got["_info"]["threads_per_cta"] == 32) == (kernel != 1)
+                        delta=delta, eps=cw.epsilon_micro, tuning=tuning)
+        assert_parity(got, ref, f"{name} {tuning} delta={delta} mode={mode}")
+        assert (got["_info"]["threads_per_cta"] == 32) == (tuning["kernel"] != 1)
+        if tuning["kernel"] != 1:  # fixed Delta = 0.1: packed option entries unless turned off
+            assert got["_info"]["packed_options"] == (1 if delta and "packed_options" not in tuning else 0)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
@@ -414,10 +416,36 @@ def test_hybrid_reward_rows(mode):
     batch = gen.concat([gen.generate(cw, 300), rel, short], cw.n_opt)
     ocfg = OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=64, max_horizon=4096)
     ref = oracle.solve(batch, ocfg, TIME)
-    got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode, delta=100_000)
-    assert got["_info"]["hybrid"] == 1 and got["_info"]["kernels_per_solve"] == 2
-    assert_parity(got, ref, f"hybrid mode={mode}")
-    np.testing.assert_array_equal(got["stats"], stats_from(got, batch))
+    for tuning in (None, dict(packed_options=2)):
+        got = gpu_solve(batch, max_tasks=64, max_opt=8, max_horizon=4096, drop_mode=mode, delta=100_000,
+                        tuning=tuning)
+        assert got["_info"]["hybrid"] == 1 and got["_info"]["kernels_per_solve"] == 2
+        assert got["_info"]["packed_options"] == (0 if tuning else 1)
+        assert_parity(got, ref, f"hybrid mode={mode} {tuning}")
+        np.testing.assert_array_equal(got["stats"], stats_from(got, batch))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_packed_option_fields_at_their_limits(mode):
+    """Packed option entries hold 16-bit fields: the largest Delta-bounded q (Delta = 489 micro:
+    q <= 2044, key up to 32703) and option lengths up to C = 4095 at H = 4096 (reward-axis addend
+    C*16 + code up to 65529).  Both axes, packed and int2 tables, equal the oracle."""
+    rng = np.random.default_rng(700 + mode)
+    tiny = gen.tiny_random(rng, 600, max_tasks=6, max_opt=8, horizon=4096)
+    tiny.deadline[:] = np.where(tiny.deadline >= 0, 4095 - (tiny.deadline * 7 % 300), tiny.deadline)
+    tiny.mand_wcet[:] = np.minimum(tiny.mand_wcet * 500, 3000)
+    tiny.opt_wcet[:] = tiny.opt_wcet * 90
+    tiny.mand_conf[:] = (tiny.mand_conf.astype(np.int64) * 7 % 400_001).astype(np.uint32)
+    tiny.opt_gain[:] = np.abs(tiny.opt_gain.astype(np.int64)) * 13 % 75_001  # R <= 1e6: q up to 2044
+    for delta in (489, 100_000):
+        ocfg = OracleConfig(drop_mode=mode, delta_micro=delta, max_tasks=6, max_horizon=4096)
+        ref = oracle.solve(tiny, ocfg, TIME)
+        for tuning in (dict(kernel=2), dict(kernel=2, packed_options=2), dict(kernel=2, axis=1),
+                       dict(kernel=2, axis=2)):
+            got = gpu_solve(tiny, max_tasks=6, max_opt=8, max_horizon=4096, drop_mode=mode, delta=delta,
+                            tuning=tuning)
+            assert got["_info"]["packed_options"] == (0 if "packed_options" in tuning else 1)
+            assert_parity(got, ref, f"packed limits delta={delta} {tuning}")
 
 
 def _remove_one(batch, rng):
