@@ -35,6 +35,9 @@
 #ifndef IC_SB_CHUNK
 #define IC_SB_CHUNK 8
 #endif
+#ifndef IC_SB_CHUNK15
+#define IC_SB_CHUNK15 8  // chunk of the 15-warp in-place kernel (128 registers)
+#endif
 #ifndef IC_BATCH_KSPLIT
 #define IC_BATCH_KSPLIT 6
 #endif
@@ -389,7 +392,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
     // chunk c reads only columns below its top, so writing it after the barrier
     // cannot disturb a lower chunk still to be computed.
-    constexpr int CH = IC_SB_CHUNK;  // groups per chunk (a multiple of 8: one decision word per 8)
+    constexpr int CH = NW == 15 ? IC_SB_CHUNK15 : IC_SB_CHUNK;  // groups per chunk (a multiple of 8: one decision word per 8)
     const int nch = d >= 0 ? (d / NT) / CH + 1 : 0;  // CTA-uniform chunk count (warp 0 has the most groups)
     for (int c = nch - 1; c >= 0; --c) {
       const int g0 = c * CH;
@@ -683,7 +686,9 @@ __device__ int tail_setup(const Params& p, const Smem& S, int64_t b, int s, int 
       int Clast = 0;
       auto option = [&](int k) {
         if (C <= (long long)d - r) {  // options that can fit (C increasing in k); only they
-          const int q = (int)(R / delta);  // bound the packed keys and the reward columns
+          // q = R div Delta in 32 bits: pass 1 bounds every prefix R to [0, 1e6] and
+          // 1 <= Delta < 2^32 (a 64-bit division is a called subroutine, 5 per option)
+          const int q = (int)((uint32_t)R / (uint32_t)delta);  // bound the packed keys and the reward columns
           qmax = max(qmax, q);
           opt_put<PK>(rp, r0 + k, make_int2((int)C, (q << 4) - (k + 1)), false);
           Clast = (int)C;

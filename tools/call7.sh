@@ -1,0 +1,21 @@
+# C4 split-phase chunk hand-off A/B; ncu summaries (r1 vs working tree on C5, C4) computed on the box
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/sum
+one() { (cd $1 && timeout 600 python bench.py --config $2 --instances ${3:-0} --no-cpu-baseline --no-e2e ${@:4} 2>/dev/null) | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1 $2 ${*:4}', round(d['value']), round(d['ms_per_step'],3), d.get('result_hash'))" 2>/dev/null || echo "$1 $2 FAILED"; }
+for rep in 1 2; do
+one . C4 0 --no-probe
+one . C4 0 --no-probe --lib ab/nosplit.so
+one . C3 0 --no-probe --tune in_place=1 --tune dp_warps=15
+one . C3 0 --no-probe --tune in_place=1 --tune dp_warps=15 --lib ab/nosplit.so
+done
+cap() {  # dir name args regex
+  (cd $1 && timeout 900 ncu --set full --import-source on --clock-control none -k regex:$4 -s 3 -c 1 -o /tmp/prof_$2 \
+    python bench.py $3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /tmp/ncu_$2.log 2>&1; echo "$2 rc=$?")
+  python tools/ncu_summary.py /tmp/prof_$2.ncu-rep $2 $5 --round r02 > gpurun_out/sum/$2.json 2>&1
+  python tools/ncu_lines.py /tmp/prof_$2.ncu-rep $1/paper_2011_01112_b200/libicsched.so ic_ 70 > gpurun_out/sum/$2_lines.txt 2>&1
+  rm -f /tmp/prof_$2.ncu-rep
+}
+cap ab/r1tree r1C5 "--config C5 --instances 400000" ic_dp_kernel 400000
+cap . C5 "--config C5 --instances 400000 --no-probe" ic_dp_kernel 400000
+cap . C4 "--config C4 --no-probe" ic_dp_kernel 10000
+ls -la gpurun_out/sum
