@@ -697,14 +697,33 @@ def main():
             f"nominal 128 B/clk/SM x {sms} SMs x {fmax:.0f} MHz (probe skipped)"
         achieved = W * BYTES_PER_EVAL / (kern_ms / 1e3) / 1e9
         traffic = None
-        prof = os.path.join(ROOT, "profiles", f"ncu_{cw.name}_summary.json")
-        if os.path.exists(prof) and not args.delta_micro:
+        prof = os.path.join(ROOT, "profiles", f"ncu_{cw.name}{'d01' if args.delta_micro == 100000 else ''}_summary.json")
+        if os.path.exists(prof) and (not args.delta_micro or args.delta_micro == 100000):
             try:
                 ps = json.load(open(prof))
                 traffic = ps.get("dram_bytes_per_instance") * n_inst
                 traffic_src = f"{os.path.relpath(prof, ROOT)} ({ps.get('round', '?')}, {ps.get('kernel', '')})"
             except Exception:
                 traffic = None
+        # issue-rate view of the same launch (the reward axis at a fixed Delta is bound by
+        # per-row and per-instance instructions, not by its evaluations): warp instructions per
+        # instance from the committed ncu capture of this workload, times the batch, over the
+        # live kernel time, against 4 warp instructions / clk / SM
+        issue = None
+        iprof = os.path.join(ROOT, "profiles", f"ncu_{cw.name}{'d01' if args.delta_micro == 100000 else ''}_summary.json")
+        if os.path.exists(iprof) and (not args.delta_micro or args.delta_micro == 100000):
+            try:
+                ps = json.load(open(iprof))
+                ipi = ps["instructions"] / ps["instances_in_capture"]
+                rate = ipi * n_inst / (kern_ms / 1e3)
+                ipeak = 4.0 * sms * fmax * 1e6
+                issue = {"achieved": rate, "peak": ipeak, "unit": "warp instructions/s", "frac": rate / ipeak,
+                         "warp_instructions_per_instance": ipi,
+                         "warp_instructions_per_32_evals": ipi / (W / n_inst / 32.0),
+                         "ncu_issue_pct": ps.get("issue_pct_of_peak"), "ncu_smem_pct": ps.get("smem_pct_of_peak"),
+                         "source": f"{os.path.relpath(iprof, ROOT)} ({ps.get('round', '?')}, {ps.get('kernel', '')})"}
+            except Exception:
+                issue = None
         line = {
             "metric": METRIC, "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -724,7 +743,8 @@ def main():
                          "work": "W_active evals x 4 B (DESIGN.md §5)",
                          "survey_evals_per_instance": W_survey / n_inst,
                          "achieved_at_survey_W": W_survey * BYTES_PER_EVAL / (kern_ms / 1e3) / 1e9},
-            "gpu_launches": args.steps,
+            "issue": issue,
+            "gpu_launches": args.steps * int(info.get("kernels_per_solve", 1)),
             "clocks": clk_s,
             "kernel": info,
             "stats": dict(zip(pkg.STATS_FIELDS, [int(x) for x in stats])),

@@ -557,7 +557,7 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
                ((uintptr_t)p.opt_gain & 15) == 0 && !h->no_vec_loads;
   const Params pw = p;  // the warp-specialised kernel's parameters
-  if (h->solo_fn && (!state || !h->hybrid)) {  // one warp per instance (ic_solo_kernel.cuh)
+  if (h->solo_fn) {  // one warp per instance (ic_solo_kernel.cuh); hybrid: then the deferred ids
     const Layout& S = h->SL;
     if (h->hybrid) {  // room for every id the solo kernel may defer, and a zeroed count
       if (in->n_instances > h->defer_cap) {

@@ -83,7 +83,7 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
   const int k0 = STATE && p.replan ? (int)mi[10] : 0;  // first row to (re)compute
   if (STATE) {
     dec = state_dec(p, bcur);
-    if (lane == 0) state_tail(p, bcur)[p.max_tasks] = rw ? 1 : 0;
+    if (lane == 0) state_tail(p, bcur)[p.max_tasks] = (rw ? 1 : 0) | 2;  // axis | written by the solo kernel
   }
   const bool refill = (int)rw != (int)mi[12];
   __syncwarp();

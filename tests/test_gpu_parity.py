@@ -471,11 +471,13 @@ def _remove_one(batch, rng):
 
 @pytest.mark.parametrize("kernel", [0, 1])
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("shape", ["C2", "tiny", "H32768"])
+@pytest.mark.parametrize("shape", ["C2", "tiny", "H32768", "hybrid"])
 def test_departures_and_arrivals(kernel, mode, shape):
     """NEXT-2 both ways (P:L112 arrivals, P:L236 departures): chained departures and arrivals
     re-planned from the state equal full solves of the changed task sets, for the solo and the
-    warp-specialised kernels, and with in-place rows at H = 32768."""
+    warp-specialised kernels, with in-place rows at H = 32768, and in the hybrid solve (C3 shape
+    at Delta = 0.1: the solo kernel keeps the reward-axis instances' state, the warp-specialised
+    kernel the deferred ones', and an instance that changes kernel between calls starts over)."""
     import paper_2011_01112_b200 as pkg
     from tests.gpu_util import to_device
     rng = np.random.default_rng(200 + mode + 10 * kernel)
@@ -485,11 +487,17 @@ def test_departures_and_arrivals(kernel, mode, shape):
     elif shape == "tiny":
         full = gen.tiny_random(rng, 1500, max_tasks=7, max_opt=3, horizon=40)
         mt, mo, H = 7, 3, 40
-    else:
+    elif shape == "H32768":
         full = gen.tiny_random(rng, 200, max_tasks=8, max_opt=3, horizon=32768, p_release=0.3)
         full.mand_wcet[:] = full.mand_wcet * 900
         full.opt_wcet[:] = full.opt_wcet * 700
         mt, mo, H = 8, 3, 32768
+    else:
+        rel = gen.tiny_random(rng, 150, max_tasks=12, max_opt=8, horizon=4096, p_release=0.6)
+        rel.mand_wcet[:] = rel.mand_wcet * 50
+        short = gen.tiny_random(rng, 150, max_tasks=12, max_opt=8, horizon=600, p_release=0.3)
+        full = gen.concat([gen.generate("C3", 60), rel, short], 8)
+        mt, mo, H = 64, 8, 4096
     full = full.select(np.nonzero(np.diff(full.task_begin) >= 4)[0])
     sc = pkg.SchedConfig(max_tasks=mt, max_opt_stages=mo, max_horizon=H, delta_micro=100_000, drop_mode=mode)
     ocfg = OracleConfig(drop_mode=mode, delta_micro=100_000, max_tasks=mt, max_horizon=H)

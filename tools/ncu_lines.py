@@ -54,6 +54,14 @@ def main():
     sub = sys.argv[3] if len(sys.argv) > 3 else "ic_"  # substring of the mangled kernel symbol
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     kname, hdr, rows = sass_rows(rep)
+    # the profiled instantiation's mangled name, e.g. "void icsched::ic_dp_kernel<(int)4, (bool)0,
+    # (bool)1>(icsched::Params)" -> "ic_dp_kernelILi4ELb0ELb1EE": the line table must come from
+    # that kernel's own code (another instantiation has other addresses)
+    m = re.search(r"::(\w+)<([^>]*)>", kname)
+    if m:
+        args = "".join(f"L{'i' if t == 'int' else 'b'}{v}E"
+                       for t, v in re.findall(r"\((int|bool)\)(-?\d+)", m.group(2)))
+        sub = f"{m.group(1)}I{args}E"
     table = line_table(lib, sub)
     kerns = sorted({k for k, _ in table})
     ia, isamp, iexe = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
