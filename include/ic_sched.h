@@ -138,6 +138,9 @@ typedef struct {
   int32_t kernel;        /* 1: warp-specialised kernel; 2: one warp per instance; default by shape          */
   int32_t packed_options;/* 2: int2 option tables in the one-warp kernel; default packed 32-bit entries when
                             a fixed Delta >= 489 micro and H <= 4096 bound every field to 16 bits      */
+  int32_t discard;       /* 1: invalidate each instance's dead decision lines in L2 after its backtrack
+                            (DRAM ~1.1x the algorithmic bytes); 2: never; default: on in the one-warp
+                            kernel, off in the warp-specialised kernel (its L2 operations cost 2.5 %) */
 } ic_sched_tuning;
 int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_tuning* tuning, ic_sched** out);
 

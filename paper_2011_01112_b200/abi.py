@@ -52,7 +52,7 @@ class SchedConfig(ctypes.Structure):
 
 
 TUNING_FIELDS = ("dp_warps", "pad_cols", "in_place", "slots", "decisions", "option_tables", "axis", "ckpt",
-                 "ctas_per_sm", "no_vec_loads", "kernel", "packed_options")
+                 "ctas_per_sm", "no_vec_loads", "kernel", "packed_options", "discard")
 
 
 class SchedTuning(ctypes.Structure):

@@ -172,6 +172,7 @@ struct ic_sched {
   int ckpt;            // re-plan checkpoint spacing (rows), power of two
   int no_vec_loads;    // 1: scalar descriptor loads only
   int solo_packed;     // the solo kernel's option tables hold packed words
+  int discard;         // tuning.discard: 0 default (solo kernel on, warp-specialised off), 1 on, 2 off
 };
 
 extern "C" int ic_sched_create(const ic_sched_config* cfg, ic_sched** out) {
@@ -192,7 +193,8 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   if (tu.dp_warps < 0 || tu.pad_cols < 0 || tu.in_place < 0 || tu.in_place > 1 || tu.slots < 0 || tu.slots > 2 ||
       tu.decisions < 0 || tu.decisions > 2 || tu.option_tables < 0 || tu.option_tables > 1 || tu.axis < 0 ||
       tu.axis > 2 || tu.ckpt < 0 || (tu.ckpt & (tu.ckpt - 1)) != 0 || tu.ctas_per_sm < 0 || tu.no_vec_loads < 0 ||
-      tu.no_vec_loads > 1 || tu.kernel < 0 || tu.kernel > 2 || tu.packed_options < 0 || tu.packed_options > 2)
+      tu.no_vec_loads > 1 || tu.kernel < 0 || tu.kernel > 2 || tu.packed_options < 0 || tu.packed_options > 2 ||
+      tu.discard < 0 || tu.discard > 2)
     return IC_ERR_INVALID_ARG;
   if (cudaSetDevice(c.device) != cudaSuccess) return IC_ERR_CUDA;
   int sms = 0;
@@ -286,6 +288,7 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
   h->axis_mode = tu.axis;
   h->ckpt = tu.ckpt ? tu.ckpt : 4;
   h->no_vec_loads = tu.no_vec_loads;
+  h->discard = tu.discard;
   if (cudaMalloc(&h->work, 16) != cudaSuccess || cudaMemset(h->work, 0, 16) != cudaSuccess) {
     free(h);
     return IC_ERR_OOM;
@@ -556,6 +559,10 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
   p.rowp_slab = h->rowp_slab;
   p.opt_vec4 = (p.smax & 3) == 0 && p.smax > 0 && ((uintptr_t)p.opt_wcet & 15) == 0 &&
                ((uintptr_t)p.opt_gain & 15) == 0 && !h->no_vec_loads;
+  // Discarding dead decision lines keeps them from HBM (C5: 64 -> 1 KB written per instance)
+  // but its L2 operations cost the warp-specialised kernel 2.5 % (C5 4.74e6 -> 4.62e6) while
+  // the one-warp kernel gains from it (C2 +3 %): default on for the solo kernel only.
+  p.discard = h->discard == 1;
   const Params pw = p;  // the warp-specialised kernel's parameters
   if (h->solo_fn) {  // one warp per instance (ic_solo_kernel.cuh); hybrid: then the deferred ids
     const Layout& S = h->SL;
@@ -576,6 +583,7 @@ static int launch_solve(ic_sched* h, const ic_batch_in* in, ic_batch_out* out, v
     p.nq = S.nq;
     p.np2 = S.np2;
     p.kp = S.kp;
+    p.discard = h->discard != 2;
     p.dec_smem = 0;
     p.dec_global = h->solo_dec;
     p.dec_slab_words = h->solo_dec_warp_words;

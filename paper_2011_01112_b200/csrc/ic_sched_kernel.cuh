@@ -35,6 +35,9 @@
 #ifndef IC_SB_CHUNK
 #define IC_SB_CHUNK 8
 #endif
+#ifndef IC_DEC_KEEP
+#define IC_DEC_KEEP 1
+#endif
 #ifndef IC_SB_CHUNK15
 #define IC_SB_CHUNK15 8  // chunk of the 15-warp in-place kernel (128 registers)
 #endif
@@ -106,6 +109,7 @@ struct Params {
   int2* rowp_g;
   int64_t rowp_slab;  // int2 per CTA slab ([2][max_tasks][kp])
   int opt_vec4;       // optional-stage rows are 16-byte aligned multiples of 4: LDG.128 loads
+  int discard;        // invalidate an instance's decision lines in L2 after its backtrack
 };
 
 __device__ __forceinline__ int32_t* state_rows(const Params& p, int64_t b) {
@@ -141,6 +145,20 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   uint32_t a;
   asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
   return a;
+}
+// Decision words are re-read by the backtrack microseconds later and then dead: they are
+// stored under an L2 evict_last policy (the policy descriptor is a compile-time constant, no
+// instruction) so the streaming descriptor and output traffic is evicted before them
+// (C5: +0.2 % throughput and 18 % fewer DRAM writes than plain stores; with the discard below,
+// DRAM traffic 1.1x the algorithmic bytes).  IC_DEC_KEEP=0 builds plain stores (A/B).
+__device__ __forceinline__ void st_dec(uint32_t* a, uint32_t v) {
+#if IC_DEC_KEEP
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+#else
+  *a = v;
+#endif
 }
 // the least column t >= first that thread tid owns (t = tid mod NT; NT need not be a power of 2)
 template <int NT>
@@ -342,7 +360,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         if (rem & 2) sub(std::integral_constant<int, 2>{});
         if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
-      decrow[(g0 >> 3) * NT + tid] = dw;
+      st_dec(&decrow[(g0 >> 3) * NT + tid], dw);
     }
   } else if constexpr (NW == 1) {
     // one warp per instance (the solo kernel), in place from high to low columns: blocks of
@@ -375,7 +393,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       if (rem & 1) dw |= blk(gtop + (rem & 6), I1{});
       if (rem & 2) dw |= blk(gtop + (rem & 4), I2{});
       if (rem & 4) dw |= blk(gtop, I4{});
-      decrow[(gtop >> 3) * NT + tid] = dw;
+      st_dec(&decrow[(gtop >> 3) * NT + tid], dw);
     }
 #pragma unroll 1
     for (int g0 = gtop - 8; g0 >= 0; g0 -= 8) {
@@ -386,7 +404,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         dw = blk(g0 + 4, I4{});
         dw |= blk(g0, I4{});
       }
-      decrow[(g0 >> 3) * NT + tid] = dw;
+      st_dec(&decrow[(g0 >> 3) * NT + tid], dw);
     }
   } else {
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
@@ -412,7 +430,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
             dw |= (uint32_t)(v[w8 + u] & 15) << (4 * u);
             nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
           }
-          decrow[((g0 + w8) >> 3) * NT + tid] = dw;
+          st_dec(&decrow[((g0 + w8) >> 3) * NT + tid], dw);
         }
       } else {
 #pragma unroll
@@ -428,7 +446,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
               nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
             }
           }
-          if (g0 + w8 < ng) decrow[((g0 + w8) >> 3) * NT + tid] = dw;
+          if (g0 + w8 < ng) st_dec(&decrow[((g0 + w8) >> 3) * NT + tid], dw);
         }
       }
     }
@@ -900,10 +918,7 @@ __device__ __forceinline__ void tail_backtrack(const Params& p, const Smem& S, i
 template <int NW>
 __device__ __forceinline__ void discard_decisions(const Params& p, const Smem& S, int s, int lane, int db) {
   constexpr int NT = 32 * NW;
-#ifdef IC_NO_DISCARD
-  return;
-#endif
-  if (p.state || p.dec_smem) return;
+  if (!p.discard || p.state || p.dec_smem) return;
   const int n = (int)S.misc[s * 16];
   const int4* inf = S.info + s * p.max_tasks;
   const char* base = (const char*)(S.dec + db * p.dec_words);

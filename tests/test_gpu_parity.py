@@ -187,6 +187,7 @@ def test_decision_placement(decisions):
                                     dict(option_tables=1, in_place=1, dp_warps=16),
                                     dict(in_place=1, dp_warps=15), dict(dp_warps=15), dict(option_tables=1, in_place=1, dp_warps=15),
                                     dict(option_tables=1, dp_warps=8, decisions=2), dict(no_vec_loads=1),
+                                    dict(discard=1), dict(kernel=2, discard=2),
                                     dict(decisions=1, dp_warps=2)])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_every_kernel_variant(tuning, mode):
