@@ -153,9 +153,13 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // DRAM traffic 1.1x the algorithmic bytes).  IC_DEC_KEEP=0 builds plain stores (A/B).
 __device__ __forceinline__ void st_dec(uint32_t* a, uint32_t v) {
 #if IC_DEC_KEEP
-  unsigned long long pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+  if (__isGlobal(a)) {  // (tuning.decisions = 1 keeps them in shared memory: a plain store)
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+  } else {
+    *a = v;
+  }
 #else
   *a = v;
 #endif
