@@ -140,7 +140,9 @@ typedef struct {
                             a fixed Delta >= 489 micro and H <= 4096 bound every field to 16 bits      */
   int32_t discard;       /* 1: invalidate each instance's dead decision lines in L2 after its backtrack
                             (DRAM ~1.1x the algorithmic bytes); 2: never; default: on in the one-warp
-                            kernel, off in the warp-specialised kernel (its L2 operations cost 2.5 %) */
+                            kernel.  The warp-specialised kernel honours it only when built with
+                            IC_WS_DISCARD=1 (the code alone costs its sweep 2 %); otherwise it never
+                            discards and the field is accepted and ignored there */
 } ic_sched_tuning;
 int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_tuning* tuning, ic_sched** out);
 

@@ -35,6 +35,11 @@
 #ifndef IC_SB_CHUNK
 #define IC_SB_CHUNK 8
 #endif
+#ifndef IC_WS_DISCARD
+// 1: the warp-specialised kernel's tail warp can discard dead decision lines (tuning.discard);
+// compiled out by default: even unexecuted, that code costs the C5 sweep 2 % (same-box A/B)
+#define IC_WS_DISCARD 0
+#endif
 #ifndef IC_DEC_KEEP
 #define IC_DEC_KEEP 1
 #endif
@@ -151,9 +156,12 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // instruction) so the streaming descriptor and output traffic is evicted before them
 // (C5: +0.2 % throughput and 18 % fewer DRAM writes than plain stores; with the discard below,
 // DRAM traffic 1.1x the algorithmic bytes).  IC_DEC_KEEP=0 builds plain stores (A/B).
-__device__ __forceinline__ void st_dec(uint32_t* a, uint32_t v) {
+__device__ __forceinline__ void st_dec(uint32_t* a, uint32_t v, bool dglob) {
 #if IC_DEC_KEEP
-  if (__isGlobal(a)) {  // (tuning.decisions = 1 keeps them in shared memory: a plain store)
+  // dglob: the launch keeps decisions in global memory (tuning.decisions = 1 puts them in shared
+  // memory: a plain store).  A uniform kernel-parameter test, not a per-store __isGlobal (QSPC),
+  // which cost the C5 sweep 2 %.
+  if (dglob) {
     unsigned long long pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
@@ -210,7 +218,7 @@ __device__ __forceinline__ void opt_put(int2* tab, size_t idx, int2 v, bool rw) 
 template <int NW, bool SB, bool DROP, int K, bool GEN, bool RW, bool PK = false>
 __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_t* __restrict__ decrow,
                                        const int4* __restrict__ ops4, const int4 (&pre)[4], const int d,
-                                       const int r, const int kr, const int lim) {
+                                       const int r, const int kr, const int lim, const bool dglob) {
   constexpr int NT = 32 * NW;
   // the solo kernel's general path loops over the options at run time, reading each from
   // shared memory (no option registers: it keeps the row loop's registers from spilling)
@@ -364,7 +372,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         if (rem & 2) sub(std::integral_constant<int, 2>{});
         if (rem & 1) sub(std::integral_constant<int, 1>{});
       }
-      st_dec(&decrow[(g0 >> 3) * NT + tid], dw);
+      st_dec(&decrow[(g0 >> 3) * NT + tid], dw, dglob);
     }
   } else if constexpr (NW == 1) {
     // one warp per instance (the solo kernel), in place from high to low columns: blocks of
@@ -397,7 +405,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
       if (rem & 1) dw |= blk(gtop + (rem & 6), I1{});
       if (rem & 2) dw |= blk(gtop + (rem & 4), I2{});
       if (rem & 4) dw |= blk(gtop, I4{});
-      st_dec(&decrow[(gtop >> 3) * NT + tid], dw);
+      st_dec(&decrow[(gtop >> 3) * NT + tid], dw, dglob);
     }
 #pragma unroll 1
     for (int g0 = gtop - 8; g0 >= 0; g0 -= 8) {
@@ -408,7 +416,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
         dw = blk(g0 + 4, I4{});
         dw |= blk(g0, I4{});
       }
-      st_dec(&decrow[(g0 >> 3) * NT + tid], dw);
+      st_dec(&decrow[(g0 >> 3) * NT + tid], dw, dglob);
     }
   } else {
     // in place, chunks of 8 groups from high to low columns, one barrier per chunk:
@@ -434,7 +442,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
             dw |= (uint32_t)(v[w8 + u] & 15) << (4 * u);
             nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
           }
-          st_dec(&decrow[((g0 + w8) >> 3) * NT + tid], dw);
+          st_dec(&decrow[((g0 + w8) >> 3) * NT + tid], dw, dglob);
         }
       } else {
 #pragma unroll
@@ -450,7 +458,7 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
               nxt[tb + (w8 + u) * NT] = stv(v[w8 + u]);
             }
           }
-          if (g0 + w8 < ng) st_dec(&decrow[((g0 + w8) >> 3) * NT + tid], dw);
+          if (g0 + w8 < ng) st_dec(&decrow[((g0 + w8) >> 3) * NT + tid], dw, dglob);
         }
       }
     }
@@ -462,14 +470,15 @@ __device__ __forceinline__ void dp_row(const int32_t* cur, int32_t* nxt, uint32_
 // general path (the solo kernel compiles K <= 9, i.e. up to 8 optional stages).
 template <int NW, bool SB, bool DROP, bool RW, int KC = 15, bool PK = false>
 __device__ __forceinline__ void dp_row_dispatch(int K, bool gen, const int32_t* cur, int32_t* nxt,
-                                                uint32_t* decrow, const int4* ops4, int d, int r, int lim) {
+                                                uint32_t* decrow, const int4* ops4, int d, int r, int lim,
+                                                bool dglob = true) {
   const int4 pre[4] = {ops4[0], ops4[1], ops4[2], ops4[3]};  // issued ahead of the K dispatch
   if (gen || K > KC) {
-    dp_row<NW, SB, DROP, KMAX, true, RW, PK>(cur, nxt, decrow, ops4, pre, d, r, K, lim);
+    dp_row<NW, SB, DROP, KMAX, true, RW, PK>(cur, nxt, decrow, ops4, pre, d, r, K, lim, dglob);
     return;
   }
 #define IC_ROW(KK) \
-  case KK: if constexpr (KK <= KC) dp_row<NW, SB, DROP, KK, false, RW, PK>(cur, nxt, decrow, ops4, pre, d, r, K, lim); break;
+  case KK: if constexpr (KK <= KC) dp_row<NW, SB, DROP, KK, false, RW, PK>(cur, nxt, decrow, ops4, pre, d, r, K, lim, dglob); break;
   switch (K) {
     IC_ROW(0) IC_ROW(1) IC_ROW(2) IC_ROW(3) IC_ROW(4) IC_ROW(5) IC_ROW(6) IC_ROW(7)
     IC_ROW(8) IC_ROW(9) IC_ROW(10) IC_ROW(11) IC_ROW(12) IC_ROW(13) IC_ROW(14) IC_ROW(15)
@@ -1088,10 +1097,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         if (p.ndec == 2) {
           bar_arrive(BAR_READY, NT + 32);  // nb sweeps into the other decision buffer
           tail_backtrack<NW>(p, S, s, lane, db);
-          discard_decisions<NW>(p, S, s, lane, db);
+          if (IC_WS_DISCARD) discard_decisions<NW>(p, S, s, lane, db);
         } else {
           tail_backtrack<NW>(p, S, s, lane, db);
-          discard_decisions<NW>(p, S, s, lane, db);
+          if (IC_WS_DISCARD) discard_decisions<NW>(p, S, s, lane, db);
           __syncwarp();
           bar_arrive(BAR_READY, NT + 32);  // decisions free: the DP warps may start nb
         }
@@ -1103,7 +1112,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       while (b < p.B) {
         bar_sync(BAR_DONE, NT + 32);
         tail_backtrack<NW>(p, S, 0, lane, 0);
-        discard_decisions<NW>(p, S, 0, lane, 0);
+        if (IC_WS_DISCARD) discard_decisions<NW>(p, S, 0, lane, 0);
         tail_outputs<NW>(p, S, 0, lane, acc);
         int64_t nb = claim();
         while (nb < p.B && tail_setup<NW>(p, S, nb, 0, lane, acc) != ST_OK) nb = claim();
@@ -1193,6 +1202,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
     const int2* ops = rpb + (size_t)k0 * kp;
     uint32_t* decrow = decb + (size_t)k0 * dec_row_words;
     const bool keep_state = p.state != nullptr;  // loop invariants, read once per instance
+    const bool dglob = !p.dec_smem || keep_state;  // decisions in global memory (hinted stores)
     const int ckm = p.ckpt - 1;
 #pragma unroll 1
     for (int pos = k0; pos < n; ++pos) {
@@ -1204,7 +1214,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
       if (rw) {
         // reward axis: columns r <= Qpre_pos; (Qpre_pos, Qpre_next] are unreachable
         dp_row_dispatch<NW, SB, DROP, true>(K, (f.y >> 9) & 1, cur, nxt, decrow, (const int4*)ops, d, 0,
-                                            auxp[pos]);
+                                            auxp[pos], dglob);
         if (keep_state && ((pos + 1) & ckm) == 0) {  // checkpoint row for later re-plans
           int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * rstride;
           for (int t = tid; t <= d; t += NT) srow[t] = nxt[t];
@@ -1220,7 +1230,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), min_blocks(NW)) ic_dp_kernel(co
         }
         int A = 0;
         if (SB) A = __reduce_max_sync(0xffffffffu, av);
-        dp_row_dispatch<NW, SB, DROP, false>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, 0);
+        dp_row_dispatch<NW, SB, DROP, false>(K, gen, cur, nxt, decrow, (const int4*)ops, d, r, 0, dglob);
         if (!SB) A = __reduce_max_sync(0xffffffffu, av);
         const int Mv = DROP ? max(M, A) : A;
         if (tid == 0) tailp[pos] = Mv & 15;
