@@ -331,8 +331,10 @@ extern "C" int ic_sched_create_tuned(const ic_sched_config* cfg, const ic_sched_
     Layout S = make_solo_layout(c, spad, hybrid ? (int)qcap : 0, packed);
     h->hybrid = hybrid ? 1 : 0;
     h->solo_packed = packed ? 1 : 0;
-    KernelFn sf = icsched::kernel_solo(drop, false, packed);
-    KernelFn sfs = icsched::kernel_solo(drop, true, packed);
+    // at most 4 optional stages: the instantiation whose unrolled sweeps stop at K = 5
+    const bool k5 = c.max_opt_stages <= 4;
+    KernelFn sf = k5 ? icsched::kernel_solo5(drop, false, packed) : icsched::kernel_solo(drop, false, packed);
+    KernelFn sfs = k5 ? icsched::kernel_solo5(drop, true, packed) : icsched::kernel_solo(drop, true, packed);
     const int bytes = S.bytes * IC_SOLO_WPC;
     int sp = 0;
     if (bytes > kSmemLimit) rc = IC_ERR_LIMIT;

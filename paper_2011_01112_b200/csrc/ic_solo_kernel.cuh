@@ -69,7 +69,7 @@ static __device__ __noinline__ int solo_setup(const Params& p, unsigned char* ba
 }
 
 // a4 + a5: the rows in place, then the optimum of row N into misc[5], misc[6].
-template <bool DROP, bool STATE, bool PK>
+template <bool DROP, bool STATE, bool PK, int KC>
 __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, uint32_t* dec, int lane) {
   // (dec: the warp's decision slab; replaced by the instance's state when one is kept)
   int32_t* const rowbuf = (int32_t*)(base + p.off_rowbuf);
@@ -120,14 +120,14 @@ __device__ __noinline__ void solo_sweep(const Params& p, unsigned char* base, ui
     const int d = f.x, K = f.y & 255;
     if (rw) {
       // reward axis: columns r <= Qpre_pos; unreachable columns above stay infinite
-      dp_row_dispatch<1, true, DROP, true, IC_SOLO_KC, PK>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
+      dp_row_dispatch<1, true, DROP, true, KC, PK>(K, (f.y >> 9) & 1, buf, buf, decrow, (const int4*)ops, d, 0, aux[pos]);
       __syncwarp();
       if (STATE && ((pos + 1) & (p.ckpt - 1)) == 0) {  // checkpoint row for later re-plans
         int32_t* srow = state_rows(p, bcur) + (int64_t)((pos + 1) / p.ckpt - 1) * (p.H + 1);
         for (int t = lane; t <= d; t += 32) srow[t] = buf[t];
       }
     } else {
-      dp_row_dispatch<1, true, DROP, false, IC_SOLO_KC, PK>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
+      dp_row_dispatch<1, true, DROP, false, KC, PK>(K, (f.y >> 8) & 1, buf, buf, decrow, (const int4*)ops, d, f.z, 0);
       __syncwarp();
       // M_pos = G_pos(d) (tail collapse); G_pos(t) = M_pos on (d, d_next] for the next row
       if (d >= 0)
@@ -197,7 +197,9 @@ static __device__ __noinline__ void solo_finish(const Params& p, unsigned char* 
 
 // STATE: the re-plan entry points (decisions and checkpoint rows kept in the caller's state);
 // plain solves run the variant without any of that code.
-template <bool DROP, bool STATE, bool PK>
+// KC: the largest option count with an unrolled sweep body; task sets with at most 4 optional
+// stages get KC = 5, whose smaller bodies leave the row loop's registers unspilled
+template <bool DROP, bool STATE, bool PK, int KC = IC_SOLO_KC>
 __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
       b = (int64_t)__shfl_sync(0xffffffffu, v, 0);
     } while (b < p.B && solo_setup<PK>(p, base, b, lane) != ST_OK);
     if (b >= p.B) break;
-    solo_sweep<DROP, STATE, PK>(p, base, dec, lane);
+    solo_sweep<DROP, STATE, PK, KC>(p, base, dec, lane);
     solo_finish<PK>(p, base, dec, lane);
   }
   __syncwarp();
@@ -230,5 +232,6 @@ __global__ void __launch_bounds__(32 * IC_SOLO_WPC, IC_SOLO_MINB) ic_solo_kernel
 }
 
 KernelFn kernel_solo(bool drop, bool state, bool packed);
+KernelFn kernel_solo5(bool drop, bool state, bool packed);
 
 }  // namespace icsched
