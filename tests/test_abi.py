@@ -86,3 +86,31 @@ def test_to_micro_quantises_like_the_spec():
         to_micro([float("nan")])
     with pytest.raises(ValueError):
         to_micro([-0.1], torch.uint32)
+
+
+def _struct_fields(header, name):
+    txt = open(os.path.join(ROOT, "include", header)).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    end = re.search(r"\}\s*" + name + ";", txt).start()
+    body = txt[txt.rindex("typedef struct {", 0, end) + len("typedef struct {"):end]
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        m = re.match(r"(u?int(?:32|64)_t)\s+(.*)", decl)
+        assert m, decl
+        fields += [(m.group(1), f.strip()) for f in m.group(2).split(",")]
+    return fields
+
+
+def test_tuning_and_info_structs_match_the_header():
+    """The binding's ctypes mirrors of ic_sched_tuning and ic_sched_info have the header's fields
+    in the header's order and widths (both grew this round: packed_options, discard)."""
+    import ctypes
+    tun = _struct_fields("ic_sched.h", "ic_sched_tuning")
+    assert [n for _, n in tun] == list(pkg.TUNING_FIELDS)
+    assert all(t == "int32_t" for t, _ in tun)
+    info = _struct_fields("ic_sched.h", "ic_sched_info")
+    got = [(n, ctypes.sizeof(t)) for n, t in pkg.SchedInfo._fields_]
+    assert got == [(n, 8 if t.endswith("64_t") else 4) for t, n in info]
